@@ -1,0 +1,189 @@
+"""Seeded, synthetic inputs shared by the oracle side and the CUDA side.
+
+This module holds NO arithmetic of the method (no derivatives, Hamiltonians,
+dissipation, time stepping).  It only states the five BASELINE.json workloads
+ as plain data and builds their initial value function
+V0 on the grid nodes, in float64, rounded once to float32 (reading A18: both
+sides start from bit-identical float32 values).
+
+Node positions follow the problem statement of PAPER.md §3.4.1 ("number
+of grid nodes, upper bound, and lower bound for each dimension, and periodic
+dimension"), with the periodic upper endpoint excluded (reading A15).  The
+target shapes are the signed-distance cylinders/spheres of PAPER.md §3.4.2
+(P:239-240).
+
+Dynamics are named by string; the oracle (oracle/) and the C-ABI binding
+(paper_2204_05520_b200/) each map the name to their own identifier.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field, replace
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+PI = math.pi
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    N: Tuple[int, ...]
+    lo: Tuple[float, ...]
+    hi: Tuple[float, ...]
+    periodic: Tuple[int, ...]
+    dynamics: str            # HOLONOMIC_BALL | HOLONOMIC_BOX | DUBINS3D | CAR4D | CAR5D | DOUBLEINT6D
+    params: Tuple[float, ...]
+    tau: Tuple[float, ...]
+    accuracy: str            # "low" (upwind1 + Euler) | "medium" (ENO2 + TVD-RK2)
+    cfl: float
+    mode: str                # "brt" | "brs"
+    target: Tuple            # ("cylinder"|"sphere", axes, radius) | ("plane", axis, sign, offset) | ("cos", axis)
+    note: str = ""
+
+    @property
+    def dims(self) -> int:
+        return len(self.N)
+
+    @property
+    def points(self) -> int:
+        return int(np.prod(self.N, dtype=np.int64))
+
+    @property
+    def periodic_mask(self) -> int:
+        m = 0
+        for d, p in enumerate(self.periodic):
+            if p:
+                m |= 1 << d
+        return m
+
+
+def _uniform_tau(T: float, k: int) -> Tuple[float, ...]:
+    return tuple(T * i / k for i in range(k + 1))
+
+
+# --- The five BASELINE.json configs; params layouts follow SURVEY.md table C-2:
+#     DUBINS3D [v, wbar, goal]; CAR4D [abar, wbar, dxbar, dybar, goal]; CAR5D [abar, alphabar, goal];
+#     DOUBLEINT6D [ubar, dbar, goal]; goal = -1 minimise (reach), +1 maximise (avoid).
+C1 = Workload(
+    name="c1", N=(41, 41, 36), lo=(-4.0, -4.0, -PI), hi=(4.0, 4.0, PI), periodic=(0, 0, 1),
+    dynamics="DUBINS3D", params=(1.0, 1.0, +1.0), tau=tuple(round(0.1 * k, 12) for k in range(21)),
+    accuracy="low", cfl=0.8, mode="brt", target=("cylinder", (0, 1), 1.0),
+    note="3D Dubins car, avoid, BRT over [0,2], 20 saves (reading A17)")
+C2 = Workload(
+    name="c2", N=(60, 60, 60, 60), lo=(-5.0, -5.0, 0.0, -PI), hi=(5.0, 5.0, 4.0, PI), periodic=(0, 0, 0, 1),
+    dynamics="CAR4D", params=(1.5, 1.0, 0.25, 0.25, -1.0), tau=(0.0, 4.0),
+    accuracy="low", cfl=0.8, mode="brt", target=("cylinder", (0, 1), 1.0),
+    note="4D car with acceleration, reach with disturbance")
+C3 = Workload(
+    name="c3", N=(40, 40, 40, 40, 40), lo=(-5.0, -5.0, -PI, 0.0, -2.0), hi=(5.0, 5.0, PI, 3.0, 2.0),
+    periodic=(0, 0, 1, 0, 0), dynamics="CAR5D", params=(1.0, 2.0, -1.0), tau=(0.0, 3.0),
+    accuracy="medium", cfl=0.5, mode="brt", target=("cylinder", (0, 1), 1.5),
+    note="5D car, reach (reading A16), ENO2 + TVD-RK2 at CFL 0.5 (reading A7)")
+C4 = Workload(
+    name="c4", N=(30,) * 6, lo=(-4.0, -2.0, -4.0, -2.0, -4.0, -2.0), hi=(4.0, 2.0, 4.0, 2.0, 4.0, 2.0),
+    periodic=(0,) * 6, dynamics="DOUBLEINT6D", params=(1.0, 0.2, -1.0), tau=(0.0, 1.0),
+    accuracy="medium", cfl=0.5, mode="brt", target=("sphere", (0, 2, 4), 1.0),
+    note="6D double integrator, 7.29e8 points, ENO2 + TVD-RK2 at CFL 0.5")
+C5_LOW = Workload(
+    name="c5-low", N=(64, 48, 48, 48, 48, 48), lo=C4.lo, hi=C4.hi, periodic=(0,) * 6,
+    dynamics="DOUBLEINT6D", params=(1.0, 0.2, -1.0), tau=(0.0, 0.5),
+    accuracy="low", cfl=0.8, mode="brt", target=("sphere", (0, 2, 4), 1.0),
+    note="6D at scale (65 GB per array): 2/4/8 GPUs only")
+C5_MED = replace(C5_LOW, name="c5-med", accuracy="medium", cfl=0.5)
+
+CONFIGS = {w.name: w for w in (C1, C2, C3, C4, C5_LOW, C5_MED)}
+
+
+def axis_nodes(N: int, lo: float, hi: float, periodic: bool) -> np.ndarray:
+    """Node positions of one axis (problem statement; reading A15)."""
+    h = (hi - lo) / (N if periodic else (N - 1))
+    return lo + h * np.arange(N, dtype=np.float64)
+
+
+def sub_box(w: Workload, axis0_range: Tuple[int, int], name: Optional[str] = None) -> Workload:
+    """The planes [a, b) of axis 0 of `w` as their own grid with identical spacing (c5-slab, reading A27)."""
+    a, b = axis0_range
+    assert not w.periodic[0]
+    x0 = axis_nodes(w.N[0], w.lo[0], w.hi[0], False)
+    N = (b - a,) + tuple(w.N[1:])
+    lo = (float(x0[a]),) + tuple(w.lo[1:])
+    hi = (float(x0[b - 1]),) + tuple(w.hi[1:])
+    return replace(w, name=name or f"{w.name}[{a}:{b}]", N=N, lo=lo, hi=hi)
+
+
+C5_SLAB_LOW = sub_box(C5_LOW, (28, 36), name="c5slab-low")
+C5_SLAB_MED = sub_box(C5_MED, (28, 36), name="c5slab-med")
+CONFIGS[C5_SLAB_LOW.name] = C5_SLAB_LOW
+CONFIGS[C5_SLAB_MED.name] = C5_SLAB_MED
+
+
+def coarsened(w: Workload, N: Sequence[int], name: Optional[str] = None, tau=None) -> Workload:
+    """Same dynamics, bounds and target on a different node count (test-sized copies)."""
+    return replace(w, name=name or f"{w.name}@{'x'.join(map(str, N))}", N=tuple(int(n) for n in N),
+                   tau=tuple(tau) if tau is not None else w.tau)
+
+
+def make_v0(w: Workload, seed: Optional[int] = None, noise: float = 1e-3) -> np.ndarray:
+    """Initial value V0 = target signed distance on the nodes, float64 -> float32 (reading A18).
+
+    seed=None gives the plain workload; an integer seed adds noise*U(-1,1) from
+    numpy.random.default_rng(seed) (the seeded parity variants of SURVEY.md §8(d)).
+    """
+    axes = [axis_nodes(n, l, h, bool(p)) for n, l, h, p in zip(w.N, w.lo, w.hi, w.periodic)]
+    kind = w.target[0]
+    shape = w.N
+    if kind in ("cylinder", "sphere"):
+        _, taxes, radius = w.target
+        acc = np.zeros((1,) * len(shape), dtype=np.float64)
+        for a in taxes:
+            s = [1] * len(shape)
+            s[a] = shape[a]
+            acc = acc + axes[a].reshape(s) ** 2
+        v = np.sqrt(acc) - radius
+    elif kind == "plane":           # signed distance to {x_axis = offset} times sign
+        _, a, sign, offset = w.target
+        s = [1] * len(shape)
+        s[a] = shape[a]
+        v = sign * (axes[a].reshape(s) - offset)
+    elif kind == "cos":
+        _, a = w.target
+        s = [1] * len(shape)
+        s[a] = shape[a]
+        v = np.cos(axes[a].reshape(s))
+    elif kind == "norm_ball":      # |x| - r over all axes (holonomic closed forms)
+        radius = w.target[1]
+        acc = np.zeros((1,) * len(shape), dtype=np.float64)
+        for a in range(len(shape)):
+            s = [1] * len(shape)
+            s[a] = shape[a]
+            acc = acc + axes[a].reshape(s) ** 2
+        v = np.sqrt(acc) - radius
+    elif kind == "random_smooth":  # sum of random low-frequency cosines (brute-force tiny grids)
+        _, rseed = w.target
+        rng = np.random.default_rng(rseed)
+        v = np.zeros((1,) * len(shape), dtype=np.float64)
+        for a in range(len(shape)):
+            s = [1] * len(shape)
+            s[a] = shape[a]
+            c = rng.uniform(0.3, 1.2)
+            ph = rng.uniform(-PI, PI)
+            v = v + rng.uniform(-1, 1) * np.cos(c * axes[a] + ph).reshape(s)
+        v = v + rng.uniform(-0.5, 0.5)
+    else:
+        raise ValueError(f"unknown target {kind}")
+    v = np.broadcast_to(v, shape).astype(np.float64)
+    if seed is not None:
+        rng = np.random.default_rng(seed)
+        v = v + noise * rng.uniform(-1.0, 1.0, size=shape)
+    return np.ascontiguousarray(v.astype(np.float32))
+
+
+def holonomic(n: int, N: int, half: float, dyn: str, params, tau, accuracy: str, mode: str = "brt",
+              target=("norm_ball", 0.5), cfl: Optional[float] = None, name: str = "holo") -> Workload:
+    """Holonomic test problems on [-half, half]^n (closed forms Z1/Z2/Z5)."""
+    return Workload(name=name, N=(N,) * n, lo=(-half,) * n, hi=(half,) * n, periodic=(0,) * n,
+                    dynamics=dyn, params=tuple(params), tau=tuple(tau), accuracy=accuracy,
+                    cfl=(0.8 if accuracy == "low" else 0.5) if cfl is None else cfl, mode=mode,
+                    target=target)

@@ -1,0 +1,226 @@
+"""NumPy "full temporaries" brute force of the time-dependent HJ step (pin Z11).
+
+TEST INFRASTRUCTURE (see oracle/__init__.py).  A second, independently written formulation of
+PAPER.md Algorithm 2 in the MATLAB style the paper contrasts itself with (Fig. 3,
+P:174-179): every temporary (ghost-padded copies, D-/D+ per axis, H, alpha) is a full N-D array.
+Differences from oracle/odp_oracle.c, on purpose:
+  * ghosts are materialised by padding the whole array per axis instead of per-node lookups;
+  * H = ext_u ext_d p.f(x,u,d) by ENUMERATING the vertices of the control and disturbance boxes
+    (Eq. 4) instead of the closed-form bang-bang choice (ball control: closed form);
+  * alpha_d = max over the achievable sign patterns of the costate (box [minD, maxD]) of
+    |f_d(x, u*, d*)|, with u*, d* again found by vertex enumeration.
+Only for tiny grids (3..7 nodes per axis).
+"""
+from __future__ import annotations
+
+import itertools
+import math
+
+import numpy as np
+
+from inputs import axis_nodes
+
+
+def _sgn(v):
+    return np.where(v >= 0, 1.0, -1.0)
+
+
+def pad(W, d, r, periodic):
+    """Return W padded with r ghost layers on both sides of axis d (readings A12, A15)."""
+    N = W.shape[d]
+    take = lambda i: np.take(W, [i], axis=d)
+    if periodic:
+        lo = np.take(W, list(range(N - r, N)), axis=d)
+        hi = np.take(W, list(range(0, r)), axis=d)
+        return np.concatenate([lo, W, hi], axis=d)
+    e0, i0 = take(0), take(1)
+    e1, i1 = take(N - 1), take(N - 2)
+    s0 = np.abs(e0 - i0) * _sgn(e0)
+    s1 = np.abs(e1 - i1) * _sgn(e1)
+    lows = [e0 + k * s0 for k in range(r, 0, -1)]     # ghost -r .. -1
+    highs = [e1 + k * s1 for k in range(1, r + 1)]    # ghost N .. N+r-1
+    return np.concatenate(lows + [W] + highs, axis=d)
+
+
+def _sl(d, ndim, a, b):
+    s = [slice(None)] * ndim
+    s[d] = slice(a, b)
+    return tuple(s)
+
+
+def derivatives(W, dx, periodic, accuracy):
+    """Full arrays D-[d], D+[d] (§3.4.4; ENO2 per reading A13)."""
+    n = W.ndim
+    Dm, Dp = [], []
+    r = 1 if accuracy == "low" else 2
+    for d in range(n):
+        Pd = pad(W, d, r, bool(periodic[d]))
+        N = W.shape[d]
+        v = {k: Pd[_sl(d, n, r + k, r + k + N)] for k in range(-r, r + 1)}
+        h = dx[d]
+        if accuracy == "low":
+            Dm.append((v[0] - v[-1]) / h)
+            Dp.append((v[1] - v[0]) / h)
+        else:
+            d2 = {j: v[j + 1] - 2.0 * v[j] + v[j - 1] for j in (-1, 0, 1)}
+            pick = lambda a, b: np.where(np.abs(a) <= np.abs(b), a, b)
+            Dm.append((v[0] - v[-1]) / h + pick(d2[-1], d2[0]) / (2.0 * h))
+            Dp.append((v[1] - v[0]) / h - pick(d2[0], d2[1]) / (2.0 * h))
+    return Dm, Dp
+
+
+# ---- dynamics as plain f(x, u, d) with explicit control/disturbance boxes ------------------------
+def model(dyn, params, n):
+    """Returns (f(X, u, d) -> list of n arrays, U vertices, D vertices, goal, ball)."""
+    p = list(params)
+    goal = p[-1]
+    if dyn == "HOLONOMIC_BALL":
+        return (lambda X, u, d: [u[k] + 0.0 * X[k] for k in range(n)]), None, [()], goal, p[0]
+    if dyn == "HOLONOMIC_BOX":
+        U = list(itertools.product(*[(-p[0], p[0])] * n))
+        D = list(itertools.product(*[(-p[1], p[1])] * n))
+        return (lambda X, u, d: [u[k] + d[k] + 0.0 * X[k] for k in range(n)]), U, D, goal, None
+    if dyn == "DUBINS3D":
+        v, wb = p[0], p[1]
+        f = lambda X, u, d: [v * np.cos(X[2]), v * np.sin(X[2]), u[0] + 0.0 * X[2]]
+        return f, [(-wb,), (wb,)], [()], goal, None
+    if dyn == "CAR4D":
+        ab, wb, dxb, dyb = p[:4]
+        f = lambda X, u, d: [X[2] * np.cos(X[3]) + d[0], X[2] * np.sin(X[3]) + d[1], u[0] + 0.0 * X[0], u[1] + 0.0 * X[0]]
+        U = list(itertools.product((-ab, ab), (-wb, wb)))
+        D = list(itertools.product((-dxb, dxb), (-dyb, dyb)))
+        return f, U, D, goal, None
+    if dyn == "CAR5D":
+        ab, alb = p[:2]
+        f = lambda X, u, d: [X[3] * np.cos(X[2]), X[3] * np.sin(X[2]), X[4] + 0.0 * X[0], u[0] + 0.0 * X[0], u[1] + 0.0 * X[0]]
+        return f, list(itertools.product((-ab, ab), (-alb, alb))), [()], goal, None
+    if dyn == "DOUBLEINT6D":
+        ub, db = p[:2]
+        f = lambda X, u, d: [X[1], u[0] + d[0] + 0.0 * X[0], X[3], u[1] + d[1] + 0.0 * X[0], X[5], u[2] + d[2] + 0.0 * X[0]]
+        return f, list(itertools.product(*[(-ub, ub)] * 3)), list(itertools.product(*[(-db, db)] * 3)), goal, None
+    raise ValueError(dyn)
+
+
+def hamiltonian(dyn, params, X, Pc):
+    """H = ext_u ext_d p.f by vertex enumeration; goal -1: min_u max_d, +1: max_u min_d (A1)."""
+    n = len(X)
+    f, U, D, goal, ball = model(dyn, params, n)
+    if ball is not None:
+        nrm = np.sqrt(sum(q * q for q in Pc))
+        return goal * ball * nrm
+    ext_u = np.minimum if goal < 0 else np.maximum
+    ext_d = np.maximum if goal < 0 else np.minimum
+    H = None
+    for u in U:
+        inner = None
+        for d in D:
+            fx = f(X, u, d)
+            val = sum(Pc[k] * fx[k] for k in range(n))
+            inner = val if inner is None else ext_d(inner, val)
+        H = inner if H is None else ext_u(H, inner)
+    return H
+
+
+def alpha(dyn, params, X, minD, maxD):
+    """alpha_d(x) = max over achievable costate sign patterns of |f_d(x, u*, d*)| (A5)."""
+    n = len(X)
+    f, U, D, goal, ball = model(dyn, params, n)
+    shape = np.broadcast(*X).shape
+    if ball is not None:
+        out = []
+        for d in range(n):
+            Md = max(abs(minD[d]), abs(maxD[d]))
+            if Md == 0:
+                out.append(np.zeros(shape))
+                continue
+            den = Md * Md
+            for e in range(n):
+                if e != d and not (minD[e] <= 0 <= maxD[e]):
+                    den += min(abs(minD[e]), abs(maxD[e])) ** 2
+            out.append(np.full(shape, ball * Md / math.sqrt(den)))
+        return out
+    signsets = []
+    for d in range(n):
+        s = []
+        if maxD[d] >= 0:
+            s.append(1.0)
+        if minD[d] < 0:
+            s.append(-1.0)
+        signsets.append(s)
+    best = [np.zeros(shape) for _ in range(n)]
+    zero = [0.0] * 3
+    for sv in itertools.product(*signsets):
+        # u* = argext_u sv.f(x,u,d) (the d-part is additive and separable), then d* likewise
+        def score(u, d):
+            fx = f(X, u, d)
+            return sum(sv[k] * fx[k] for k in range(n))
+        d_any = D[0]
+        cand = [(u, score(u, d_any)) for u in U]
+        # pointwise arg-ext over vertices
+        ustar_score = cand[0][1]
+        ustar_idx = np.zeros(shape, dtype=int)
+        for i, (u, sc) in enumerate(cand[1:], start=1):
+            better = sc > ustar_score if goal > 0 else sc < ustar_score
+            ustar_idx = np.where(better, i, ustar_idx)
+            ustar_score = np.where(better, sc, ustar_score)
+        u_any = U[0]
+        candd = [(d, score(u_any, d)) for d in D]
+        dstar_score = candd[0][1]
+        dstar_idx = np.zeros(shape, dtype=int)
+        for i, (d, sc) in enumerate(candd[1:], start=1):
+            better = sc < dstar_score if goal > 0 else sc > dstar_score
+            dstar_idx = np.where(better, i, dstar_idx)
+            dstar_score = np.where(better, sc, dstar_score)
+        for iu, u in enumerate(U):
+            for idd, d in enumerate(D):
+                mask = (ustar_idx == iu) & (dstar_idx == idd)
+                if not mask.any():
+                    continue
+                fx = f(X, u, d)
+                for k in range(n):
+                    best[k] = np.where(mask, np.maximum(best[k], np.abs(np.broadcast_to(fx[k], shape))), best[k])
+    return best
+
+
+def solve(w, V0, cfl=None, store_initial=False):
+    """Whole solve in full-temporaries style; returns (snapshots at tau[1:], steps)."""
+    n = w.dims
+    dx = [(h - l) / (N if p else N - 1) for N, l, h, p in zip(w.N, w.lo, w.hi, w.periodic)]
+    axes = [axis_nodes(N, l, h, bool(p)) for N, l, h, p in zip(w.N, w.lo, w.hi, w.periodic)]
+    X = np.meshgrid(*axes, indexing="ij")
+    C = cfl if cfl is not None else w.cfl
+    V = V0.astype(np.float64).copy()
+    T = V0.astype(np.float64)
+
+    def L_of(W):
+        Dm, Dp = derivatives(W, dx, w.periodic, w.accuracy)
+        minD = [min(Dm[d].min(), Dp[d].min()) for d in range(n)]
+        maxD = [max(Dm[d].max(), Dp[d].max()) for d in range(n)]
+        Pc = [(Dm[d] + Dp[d]) / 2.0 for d in range(n)]
+        H = hamiltonian(w.dynamics, w.params, X, Pc)
+        A = alpha(w.dynamics, w.params, X, minD, maxD)
+        L = H + sum(A[d] * (Dp[d] - Dm[d]) / 2.0 for d in range(n))
+        amax = [float(A[d].max()) for d in range(n)]
+        return L, amax
+
+    t, steps, outs = 0.0, 0, []
+    eps = 1e-12 * max(1.0, w.tau[-1])
+    for k in range(1, len(w.tau)):
+        while w.tau[k] - t > eps:
+            L, amax = L_of(V)
+            s = sum(a / h for a, h in zip(amax, dx))
+            dt = C / s if s > 0 else w.tau[k] - t
+            dt = min(dt, w.tau[k] - t)
+            if w.accuracy == "low":
+                Vn = V + dt * L
+            else:
+                V1 = V + dt * L
+                L1, _ = L_of(V1)
+                Vn = 0.5 * (V + (V1 + dt * L1))
+            if w.mode == "brt":
+                Vn = np.minimum(Vn, T)
+            V = Vn
+            t += dt
+            steps += 1
+        outs.append(V.copy())
+    return np.stack(outs), steps
