@@ -1,0 +1,295 @@
+"""bench.py -- grid-point updates/s per RK stage of the B200 HJ level-set step (BASELINE.json metric).
+
+A "step" is one complete odp_hj_solve of the workload: every row of SURVEY.md §8(a) (derivatives,
+range reduction, alpha/CFL finalize, Hamiltonian + dissipation + RK stage + BRT min, tau loop,
+snapshot) over the whole grid.  value = points x RK stages / device time.
+
+N=1 workload: c4 (6D double integrator, 30^6 = 7.29e8 points, ENO2 + TVD-RK2, BRT over [0,1]) --
+the largest config that fits one GPU and the one BASELINE.json's scaling target names.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "grid-point updates/s per RK stage"
+UNIT = "point-stages/s"
+
+# algorithmic HBM bytes per point of one launch (SURVEY.md §8(a) table "Bytes per point per stage")
+PASS1_BYTES = 4                                     # read W
+PASS2_BYTES = {("low", "brt"): 12, ("low", "brs"): 8,          # Euler: R W, (R V0), W V'
+               ("medium", "brt"): 12, ("medium", "brs"): 10}   # mean of RK stage 1 (8) and stage 2 (16 / 12)
+STAGE_BYTES = {("low", "brt"): 16, ("low", "brs"): 12, ("medium", "brt"): 16, ("medium", "brs"): 14}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# --------------------------------------------------------------------------------------------------
+# CPU baseline / reference arm: the float64 oracle as it stands, on a bounded sample of the workload
+# --------------------------------------------------------------------------------------------------
+def oracle_sample(w, target_s: float = 15.0):
+    """Time the oracle (as it stands) on a centred sub-box of the workload with the same spacing,
+    dynamics and target, for exactly one time step; the box is sized so the run takes about
+    target_s seconds.  Returns (point-stages/s, sample description, cores, seconds, point-stages)."""
+    import oracle
+    from inputs import make_v0
+    cores = oracle.max_threads()
+
+    def box(side):
+        N = tuple(min(side, n) for n in w.N)
+        lo, hi = [], []
+        for n_full, n, l, h, p in zip(w.N, N, w.lo, w.hi, w.periodic):
+            dx = (h - l) / (n_full if p else n_full - 1)
+            c0 = (n_full - n) // 2
+            lo.append(l + c0 * dx)
+            hi.append(l + (c0 + n - (0 if p else 1)) * dx)
+        return w.__class__(**{**w.__dict__, "N": N, "lo": tuple(lo), "hi": tuple(hi)})
+
+    def timed(sub):
+        V0 = make_v0(sub)
+        L, mn, mx, amax, _, _ = oracle.stage(V0, sub.lo, sub.hi, sub.periodic_mask, sub.dynamics, sub.params,
+                                             sub.accuracy)
+        dx = [(h - l) / (n if p else n - 1) for n, l, h, p in zip(sub.N, sub.lo, sub.hi, sub.periodic)]
+        dt = oracle.cfl_dt(amax, dx, sub.cfl)
+        one = sub.__class__(**{**sub.__dict__, "tau": (0.0, dt)})       # exactly one CFL step
+        t0 = time.perf_counter()
+        r = oracle.solve_workload(one, V0=V0, raise_on_error=False)
+        return time.perf_counter() - t0, int(np.prod(sub.N)) * r.stages, r.stages
+
+    side = 10
+    el, work, stages = timed(box(side))
+    n = len(w.N)
+    side = int(side * (target_s / max(el, 1e-3)) ** (1.0 / n))
+    side = max(6, min(side, max(w.N)))
+    sub = box(side)
+    el, work, stages = timed(sub)
+    sample = (f"oracle float64 on a {'x'.join(map(str, sub.N))} centred sub-box of {w.name} (same spacing, "
+              f"dynamics, target), one time step = {stages} RK stages, {el:.1f} s")
+    return work / el, sample, cores, el, work
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+        if rank != 0:
+            dist.barrier()
+            return
+    from inputs import CONFIGS
+    w = CONFIGS[args.config]
+    times, work = [], []
+    for i in range(args.warmup + args.steps):
+        rate, sample, cores, el, pts = oracle_sample(w, target_s=args.ref_seconds)
+        if i >= args.warmup:
+            times.append(el)
+            work.append(pts)
+    value = sum(work) / sum(times)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": w.name, "grid": list(w.N), "accuracy": w.accuracy,
+                                             "mode": w.mode},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# --------------------------------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import paper_2204_05520_b200 as odp
+    from inputs import CONFIGS, make_v0
+    rank, world, local = dist_env()
+    if world > 1:
+        from paper_2204_05520_b200 import dist as odist
+        return odist.bench_main(args)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    w = CONFIGS[args.config]
+    V0h = make_v0(w)
+    V0 = torch.from_numpy(V0h).to(dev)
+    g = odp.Grid(w.N, w.lo, w.hi, w.periodic_mask)
+    nout = len(w.tau) - 1
+    out = torch.empty((nout,) + w.N, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def one(timing=False):
+        return odp.hj_solve(g, w.dynamics, w.params, V0, w.tau, w.accuracy, w.mode, out=out, cfl=w.cfl,
+                            kernel=args.kernel, stream=stream, timing=timing)[1]
+
+    for _ in range(args.warmup):
+        info = one()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kms = {"pass1": 0.0, "pass2": 0.0, "control": 0.0}
+    launches = 0
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            info = one(timing=True)
+            for k in kms:
+                kms[k] += info["kernel_ms"][k]
+            launches += g.launch_count()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    clocks = clk.summary()
+    total_ms = e0.elapsed_time(e1)
+    P = w.points
+    stages = info["stages"]
+    value = P * stages * args.steps / (total_ms / 1e3)
+
+    # end to end through the C-ABI host entry point: pinned host V0 -> device -> solve -> host out
+    V0p = torch.from_numpy(V0h).pin_memory()
+    outp = torch.empty((nout,) + w.N, dtype=torch.float32).pin_memory()
+    odp.hj_solve_host(g, w.dynamics, w.params, V0p, w.tau, w.accuracy, w.mode, out=outp, cfl=w.cfl,
+                      kernel=args.kernel)
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 3))
+    for _ in range(e2e_steps):
+        odp.hj_solve_host(g, w.dynamics, w.params, V0p, w.tau, w.accuracy, w.mode, out=outp, cfl=w.cfl,
+                          kernel=args.kernel)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_value = P * stages / e2e_s
+
+    peak, peak_kind = measured_peaks()
+    key = (w.accuracy, w.mode)
+    n_pass2 = stages * args.steps       # one pass-2 launch per stage
+    pass2_ms = kms["pass2"] / n_pass2
+    pass1_ms = kms["pass1"] / n_pass2
+    achieved = PASS2_BYTES[key] * P / (pass2_ms / 1e3) / 1e9
+    stage_gbs = STAGE_BYTES[key] * P / ((pass1_ms + pass2_ms) / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(f"{w.name}:pass2")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": w.name, "grid": list(w.N), "points": P, "dynamics": w.dynamics,
+                   "accuracy": w.accuracy, "mode": w.mode, "cfl": w.cfl, "tau": [w.tau[0], w.tau[-1]],
+                   "rk_stages_per_step": stages, "time_steps_per_step": info["steps"], "kernel": args.kernel,
+                   "l2": "inputs larger than L2 (2 x 2.9 GB working arrays)" if P * 4 > 126e6 else "fits L2",
+                   "parallelism": "single GPU"},
+        "roofline": {"bound": "hbm", "kernel": "pass2 (D+-, H, dissipation, RK stage, BRT min)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_kind": peak_kind,
+                     "bytes_per_point": PASS2_BYTES[key], "avg_launch_ms": pass2_ms,
+                     "stage": {"bytes_per_point": STAGE_BYTES[key], "achieved": stage_gbs,
+                               "frac": stage_gbs / peak, "pass1_ms": pass1_ms}},
+        "clocks": clocks,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": P * 4, "d2h_bytes_per_step": P * 4 * nout},
+        "gpu_launches": launches,
+        "kernel_ms_share": {k: v / max(total_ms, 1e-9) for k, v in kms.items()},
+    }
+    if not args.no_cpu_baseline:
+        rate, sample, cores, el, pts = oracle_sample(w, target_s=args.ref_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+    print(json.dumps(line), flush=True)
+    g.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "generic", "tiled"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

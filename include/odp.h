@@ -1,0 +1,146 @@
+/*
+ * include/odp.h -- C-ABI of the B200-native time-dependent Hamilton-Jacobi level-set step
+ * (OptimizedDP, Bui et al., arXiv 2204.05520).  Implemented by paper_2204_05520_b200/libodp.so
+ * (hand-written sm_100a CUDA kernels + a C++ host orchestrator).
+ *
+ * What the library computes (§3.2, Eq. 4):
+ *     D_s phi(z,s) + H(z, grad phi) = 0,  H = min_d max_u grad(phi)^T f(z,u,d),  phi(z,0) = phi0(z)
+ * solved backward in time (tau = -s >= 0, V_tau = H) by the level-set algorithm of Algorithm 2
+ * (P:146-172): per node one-sided derivatives (§3.4.4), optimal control/disturbance and
+ * Hamiltonian (l.153-156), global derivative range (l.157-158), Lax-Friedrichs dissipation with
+ * alpha_i (l.160-164, dissipation sign per DESIGN.md reading A2), CFL time step (l.167, §3.4.3
+ * P:243), Runge-Kutta update (l.169); BRT = min with the target after every full step (reading
+ * A11).  The grid follows §3.4.1.  Every reading of the paper is listed in DESIGN.md §3.
+ *
+ * Conventions for every function:
+ *   - returns odp_status; never throws across the ABI; on failure odp_last_error() holds a
+ *     message (thread-local, valid until the next call from the same thread);
+ *   - arrays are row-major with axis 0 outermost and axis dims-1 contiguous (§4.1);
+ *   - value arrays are float32; coordinates, bounds, params and times are float64.
+ */
+#ifndef ODP_H_
+#define ODP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    ODP_OK = 0,
+    ODP_EINVAL = 1,    /* argument validation failed (before any device work)              */
+    ODP_ENUMERIC = 2,  /* NaN or max|V| > 1e10 in a stage input (reading A19)   */
+    ODP_ECUDA = 3,     /* a CUDA runtime call or kernel launch failed                       */
+    ODP_ENCCL = 4,     /* reserved for the multi-GPU transport                               */
+    ODP_ENOMEM = 5     /* device or host allocation failed                                   */
+} odp_status;
+
+typedef enum {
+    ODP_LOW = 1,       /* first-order upwind derivatives + forward Euler (stencil radius 1)  */
+    ODP_MEDIUM = 2     /* second-order ENO derivatives + TVD-RK2 (Heun)  (stencil radius 2)  */
+} odp_accuracy;
+
+typedef enum { ODP_BRS = 0, ODP_BRT = 1 } odp_mode;
+
+/* Compiled-in dynamics.  params layouts (doubles); goal = -1 to
+ * minimise (reach), +1 to maximise (avoid); the disturbance always takes the opposite goal:
+ *   HOLONOMIC_BALL [ubar, goal]                xdot = u, |u|_2 <= ubar          (any dims)
+ *   HOLONOMIC_BOX  [ubar, dbar, goal]          xdot_i = u_i + d_i              (any dims)
+ *   DUBINS3D       [v, wbar, goal]             (x, y, th): v cos th, v sin th, w
+ *   CAR4D          [abar, wbar, dxbar, dybar, goal]  (x, y, v, th): v cos th + dx, v sin th + dy, a, w
+ *   CAR5D          [abar, alphabar, goal]      (x, y, th, v, w): v cos th, v sin th, w, a, alpha
+ *   DOUBLEINT6D    [ubar, dbar, goal]          (px, vx, py, vy, pz, vz): v_i, u_i + d_i        */
+typedef enum {
+    ODP_DYN_HOLONOMIC_BALL = 0,
+    ODP_DYN_HOLONOMIC_BOX = 1,
+    ODP_DYN_DUBINS3D = 2,
+    ODP_DYN_CAR4D = 3,
+    ODP_DYN_CAR5D = 4,
+    ODP_DYN_DOUBLEINT6D = 5
+} odp_dynamics;
+
+/* Kernel family used for the two passes of every stage. */
+typedef enum {
+    ODP_KERNEL_AUTO = 0,     /* stream, else tiled, else generic -- whichever covers the grid */
+    ODP_KERNEL_GENERIC = 1,  /* one thread per node, neighbours through L1/L2                 */
+    ODP_KERNEL_TILED = 2,    /* inner-plane tile + every outer neighbour tile staged in shared
+                                memory by 1-D TMA bulk copies (mbarrier pipeline)             */
+    ODP_KERNEL_STREAM = 3    /* CTA marches the innermost outer axis with a register window;
+                                in-plane tile in padded shared memory                          */
+} odp_kernel;
+
+typedef struct odp_grid odp_grid;   /* opaque; one solve at a time per handle */
+
+typedef struct {
+    double cfl;               /* CFL factor C; <= 0 selects the default 0.8 (LOW) / 0.5 (MEDIUM) (A7) */
+    const float *target;      /* BRT min operand (device, same layout as V0); NULL -> V0.  Separate
+                                 from V0 so a solve can restart from a snapshot    */
+    void *stream;             /* cudaStream_t to run on; NULL -> the library's own stream          */
+    int write_initial;        /* 1 -> out holds ntau slices, out[0] = V0; 0 -> ntau-1 slices       */
+    int kernel;               /* odp_kernel                                                         */
+    int use_graph;            /* 1 -> replay the per-step launch sequence as a CUDA graph          */
+    double *tau_reached;      /* optional out: tau at return (valid on ODP_ENUMERIC too)            */
+    long long *steps_taken;   /* optional out: time steps taken                                     */
+    long long *stages_taken;  /* optional out: RK stages evaluated                                  */
+    double *kernel_ms;        /* optional out [3]: summed device time of pass 1, pass 2, finalize   */
+} odp_solve_opts;
+
+/*
+ * odp_grid_create -- Cartesian grid of §3.4.1: node counts N[d], bounds [lo[d], hi[d]]
+ * and a periodic bit per axis (bit d of periodic_mask).  Spacing (hi-lo)/(N-1), or (hi-lo)/N on
+ * periodic axes whose upper endpoint is excluded (reading A15).  Host pointers, copied.
+ * Errors: ODP_EINVAL if dims is not in 1..6, any N[d] < 3, or lo[d] >= hi[d].
+ * Ownership: the caller destroys the handle with odp_grid_destroy.
+ */
+odp_status odp_grid_create(int dims, const double *lo, const double *hi, const int64_t *N,
+                           uint32_t periodic_mask, odp_grid **out);
+
+/* Frees the handle and the device working buffers it caches.  NULL is ignored. */
+void odp_grid_destroy(odp_grid *g);
+
+/* Copies dims, N[0..dims), the spacing dx[0..dims) and the point count (any out pointer may be NULL). */
+odp_status odp_grid_info(const odp_grid *g, int *dims, int64_t *N, double *dx, int64_t *points);
+
+/*
+ * odp_hj_solve -- solve Eq. 4 from V0 through the save times tau[0..ntau) (tau[0] = 0, strictly
+ * increasing, float64 host array) on the current CUDA device.
+ *   dynamics_id, params, nparams  a compiled-in functor and its parameters (host doubles)
+ *   V0       DEVICE pointer, points() float32 values: phi0 on the nodes (initial value and, unless
+ *            opts->target is given, the BRT target)
+ *   accuracy ODP_LOW | ODP_MEDIUM;  mode ODP_BRS | ODP_BRT
+ *   out      DEVICE pointer, (ntau-1) x points() floats (ntau x points() with write_initial):
+ *            out[k] = V(tau[k+1]).  Must not alias V0.
+ *   opts     nullable.
+ * Ownership: caller owns V0, out, params, tau, target; the library owns its working buffers.
+ * Errors: ODP_EINVAL (bad ids, param count, dims mismatch with the functor, ntau < 2, tau[0] != 0,
+ * unsorted tau, NULL pointers); ODP_ENUMERIC (NaN or |V| > 1e10 in a stage input -- snapshots up
+ * to the last completed save time are valid and tau_reached is set); ODP_ECUDA; ODP_ENOMEM.
+ * The call returns after the device work has completed (it synchronises its stream).
+ */
+odp_status odp_hj_solve(odp_grid *g, int dynamics_id, const double *params, int nparams,
+                        const float *V0, const double *tau, int ntau, int accuracy, int mode,
+                        float *out, const odp_solve_opts *opts);
+
+/*
+ * odp_hj_solve_host -- as odp_hj_solve, but V0, out and opts->target are HOST pointers.  The
+ * library allocates device copies, copies V0 (and target) in, solves, and copies every snapshot
+ * back to `out` before returning (the end-to-end path; pinned host memory is fastest).
+ */
+odp_status odp_hj_solve_host(odp_grid *g, int dynamics_id, const double *params, int nparams,
+                             const float *V0, const double *tau, int ntau, int accuracy, int mode,
+                             float *out, const odp_solve_opts *opts);
+
+/* Number of kernel launches issued by the last solve on this handle (launch accounting). */
+long long odp_last_launch_count(const odp_grid *g);
+
+/* Human-readable message for the last failing call on this thread ("" if none). */
+const char *odp_last_error(void);
+
+/* Library version string, e.g. "odp-b200 0.1 sm_100a". */
+const char *odp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ODP_H_ */

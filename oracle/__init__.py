@@ -59,7 +59,8 @@ def lib():
         _lib.oracle_alpha.argtypes = [c_int, D, c_int, c_int, D, D, D, D]
         _lib.oracle_stage.argtypes = [c_int, I64, D, D, c_u32, c_int, D, c_int, D, c_int, D, D, c_int]
         _lib.oracle_hj_solve.argtypes = [c_int, I64, D, D, c_u32, c_int, D, c_int, F, F, D, c_int, c_int,
-                                         c_int, c_dbl, c_int, c_int, D, D, D, I64, I64, c_int]
+                                         c_int, c_dbl, c_int, c_int, D, D, D, I64, I64, c_int,
+                                         ctypes.c_void_p]
         _lib.oracle_max_threads.restype = c_int
         _lib.oracle_cfl_dt.argtypes = [c_int, D, D, c_dbl, c_dbl]
         _lib.oracle_cfl_dt.restype = c_dbl
@@ -199,7 +200,7 @@ class SolveResult:
 
 def hj_solve(N, lo, hi, periodic_mask: int, dyn: str, params, V0, tau: Sequence[float], accuracy: str,
              mode: str, cfl: float = 0.0, target=None, write_initial: bool = False, store_f32: bool = False,
-             amax_fixed=None, nthreads: int = 0, raise_on_error: bool = True) -> SolveResult:
+             amax_fixed=None, nthreads: int = 0, raise_on_error: bool = True, ambiguity: bool = False) -> SolveResult:
     """Full oracle solve (O0-O9). V0/target float32 arrays of shape N; returns float64 snapshots."""
     N = tuple(int(v) for v in N)
     n = len(N)
@@ -217,6 +218,7 @@ def hj_solve(N, lo, hi, periodic_mask: int, dyn: str, params, V0, tau: Sequence[
     amf = None
     if amax_fixed is not None:
         amf = np.ascontiguousarray(amax_fixed, dtype=np.float64)
+    amb = np.zeros(N, dtype=np.uint8) if ambiguity else None
     tr = ctypes.c_double()
     steps = ctypes.c_int64()
     stages = ctypes.c_int64()
@@ -226,10 +228,13 @@ def hj_solve(N, lo, hi, periodic_mask: int, dyn: str, params, V0, tau: Sequence[
                                tgt.ctypes.data_as(Fp) if tgt is not None else None, tp, len(ta),
                                ACC_IDS[accuracy], MODE_IDS[mode], float(cfl), int(write_initial), int(store_f32),
                                amf.ctypes.data_as(Dp) if amf is not None else None, out.ctypes.data_as(Dp),
-                               ctypes.byref(tr), ctypes.byref(steps), ctypes.byref(stages), int(nthreads))
+                               ctypes.byref(tr), ctypes.byref(steps), ctypes.byref(stages), int(nthreads),
+                               amb.ctypes.data if amb is not None else None)
     if st and raise_on_error:
         raise OracleError(st)
-    return SolveResult(out, tr.value, steps.value, stages.value, st)
+    r = SolveResult(out, tr.value, steps.value, stages.value, st)
+    r.ambiguous = amb
+    return r
 
 
 def solve_workload(w, V0=None, seed=None, **kw) -> SolveResult:

@@ -110,8 +110,14 @@ static double eno_pick(double a, double b) { return fabs(a) <= fabs(b) ? a : b; 
 
 /* One-sided derivatives D-, D+ along axis d at node (idx, flat) -- §3.4.4.
  * LOW: first-order upwind differences.  MEDIUM: second-order ENO. */
+/* ENO2 decision ambiguity (test support, reading A28): a pick whose two candidates are within
+ * float32 evaluation noise of each other in magnitude (| |a| - |b| | <= 2e-5) while differing in
+ * value (|a - b| > 2e-4, i.e. opposite signs) can legitimately go either way in a float32
+ * evaluation; such nodes are reported so parity tests can exempt them. */
+static int eno_ambiguous(double a, double b) { return fabs(fabs(a) - fabs(b)) <= 2e-5 && fabs(a - b) > 2e-4; }
+
 static void og_deriv(const og *g, const double *W, const int64_t *idx, int64_t flat, int d, int acc,
-                     double *dm, double *dp) {
+                     double *dm, double *dp, unsigned char *amb) {
     const int64_t i = idx[d];
     const int64_t base = flat - i * g->stride[d];
     const double h = g->dx[d];
@@ -127,6 +133,7 @@ static void og_deriv(const og *g, const double *W, const int64_t *idx, int64_t f
         const double dd_p = v0 - 2.0 * vp1 + vp2;  /* delta^2 at i+1 */
         *dm = (v0 - vm1) / h + eno_pick(dd_m, dd_0) / (2.0 * h);
         *dp = (vp1 - v0) / h - eno_pick(dd_0, dd_p) / (2.0 * h);
+        if (amb && (eno_ambiguous(dd_m, dd_0) || eno_ambiguous(dd_0, dd_p))) *amb = 1;
     }
 }
 
@@ -312,7 +319,7 @@ static void idx_of_row(const og *g, int64_t row, int64_t *idx) {
 }
 
 static void og_stage(const og *g, const ofun *f, const double *W, int acc, const double *amax_fixed,
-                     double *L, ostage *st) {
+                     double *L, ostage *st, unsigned char *amb) {
     const int n = g->n;
     const int64_t Nl = g->N[n - 1], rows = g->P / Nl;
     for (int d = 0; d < n; ++d) { st->minD[d] = INFINITY; st->maxD[d] = -INFINITY; st->amax[d] = 0.0; }
@@ -335,7 +342,7 @@ static void og_stage(const og *g, const ofun *f, const double *W, int acc, const
                 if (fabs(w) > mabs) mabs = fabs(w);
                 for (int d = 0; d < n; ++d) {
                     double dm, dp;
-                    og_deriv(g, W, idx, flat, d, acc, &dm, &dp);
+                    og_deriv(g, W, idx, flat, d, acc, &dm, &dp, NULL);
                     mn[d] = fmin(mn[d], fmin(dm, dp));   /* l.157 */
                     mx[d] = fmax(mx[d], fmax(dm, dp));   /* l.158 */
                 }
@@ -363,7 +370,7 @@ static void og_stage(const og *g, const ofun *f, const double *W, int acc, const
                 const int64_t flat = row * Nl + j;
                 for (int d = 0; d < n; ++d) {
                     x[d] = g->x[d][idx[d]];
-                    og_deriv(g, W, idx, flat, d, acc, &dm[d], &dp[d]);  /* l.153 */
+                    og_deriv(g, W, idx, flat, d, acc, &dm[d], &dp[d], amb ? amb + flat : NULL);  /* l.153 */
                     p[d] = 0.5 * (dm[d] + dp[d]);                       /* A3 */
                 }
                 double H = of_ham(f, x, p);                             /* l.154-156 */
@@ -439,7 +446,7 @@ int oracle_derivs(int n, const int64_t *N, const double *lo, const double *hi, u
     for (int64_t flat = 0; flat < g.P; ++flat) {
         int64_t r = flat;
         for (int d = n - 1; d >= 0; --d) { idx[d] = r % g.N[d]; r /= g.N[d]; }
-        for (int d = 0; d < n; ++d) og_deriv(&g, W, idx, flat, d, acc, &Dm[d * g.P + flat], &Dp[d * g.P + flat]);
+        for (int d = 0; d < n; ++d) og_deriv(&g, W, idx, flat, d, acc, &Dm[d * g.P + flat], &Dp[d * g.P + flat], NULL);
     }
     og_free(&g);
     return OR_OK;
@@ -496,7 +503,7 @@ int oracle_stage(int n, const int64_t *N, const double *lo, const double *hi, ui
     if (nthreads > 0) omp_set_num_threads(nthreads);
 #endif
     ostage s;
-    og_stage(&g, &f, W, acc, NULL, L, &s);
+    og_stage(&g, &f, W, acc, NULL, L, &s, NULL);
     for (int d = 0; d < n; ++d) { range_out[d] = s.minD[d]; range_out[n + d] = s.maxD[d]; range_out[2 * n + d] = s.amax[d]; }
     range_out[3 * n] = s.maxabs;
     range_out[3 * n + 1] = s.nan;
@@ -513,13 +520,14 @@ int oracle_stage(int n, const int64_t *N, const double *lo, const double *hi, ui
  *   out          (ntau-1) x P doubles (write_initial=0) or ntau x P (write_initial=1)
  *   store_f32    1 -> round V to float32 after every stage (precision-conditioning pin Z4)
  *   amax_fixed   non-NULL -> alpha^max used for dt (windowed oracle, pin Z12)
+ *   amb_out      non-NULL -> P bytes, OR over all stages of the ENO2 decision ambiguity flag
  * Returns OR_OK, OR_EINVAL, OR_ENUMERIC (tau_reached/steps valid), OR_ENOMEM.
  */
 int oracle_hj_solve(int n, const int64_t *N, const double *lo, const double *hi, uint32_t pmask,
                     int dyn, const double *prm, int np, const float *V0, const float *target,
                     const double *tau, int ntau, int acc, int mode, double cfl, int write_initial,
                     int store_f32, const double *amax_fixed, double *out, double *tau_reached,
-                    int64_t *steps_taken, int64_t *stages_taken, int nthreads) {
+                    int64_t *steps_taken, int64_t *stages_taken, int nthreads, unsigned char *amb_out) {
     og g;
     ofun f;
     int st = og_init(&g, n, N, lo, hi, pmask);
@@ -553,7 +561,7 @@ int oracle_hj_solve(int n, const int64_t *N, const double *lo, const double *hi,
 
     for (int k = 1; k < ntau && status == OR_OK; ++k) {
         while (tau[k] - t > eps) {                                    /* O2 */
-            og_stage(&g, &f, V, acc, amax_fixed, L, &s);             /* O3 */
+            og_stage(&g, &f, V, acc, amax_fixed, L, &s, amb_out);   /* O3 */
             ++stages;
             if (guard_bad(&s)) { status = OR_ENUMERIC; break; }
             const double dt = og_dt(n, s.amax, g.dx, cfl, tau[k] - t);   /* O4 */
@@ -571,7 +579,7 @@ int oracle_hj_solve(int n, const int64_t *N, const double *lo, const double *hi,
                     double v = V[i] + dt * L[i];
                     V1[i] = store_f32 ? round_f32(v) : v;
                 }
-                og_stage(&g, &f, V1, acc, amax_fixed, L, &s);          /* A8: own range, dt kept */
+                og_stage(&g, &f, V1, acc, amax_fixed, L, &s, amb_out);  /* A8: own range, dt kept */
                 ++stages;
                 if (guard_bad(&s)) { status = OR_ENUMERIC; break; }
 #pragma omp parallel for schedule(static)

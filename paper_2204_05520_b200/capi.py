@@ -1,0 +1,220 @@
+"""Thin ctypes binding of include/odp.h (argument marshalling only; every step runs in libodp.so).
+
+The product path never falls back to anything else: if libodp.so is missing, importing this
+module raises.  Torch supplies device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("ODP_LIB_PATH") or os.path.join(HERE, "libodp.so")
+
+ODP_OK, ODP_EINVAL, ODP_ENUMERIC, ODP_ECUDA, ODP_ENCCL, ODP_ENOMEM = 0, 1, 2, 3, 4, 5
+ACCURACY = {"low": 1, "medium": 2}
+MODE = {"brs": 0, "brt": 1}
+KERNEL = {"auto": 0, "generic": 1, "tiled": 2, "stream": 3}
+DYNAMICS = {"HOLONOMIC_BALL": 0, "HOLONOMIC_BOX": 1, "DUBINS3D": 2, "CAR4D": 3, "CAR5D": 4, "DOUBLEINT6D": 5}
+
+# every symbol include/odp.h declares (checked by tests/test_capi_host.py)
+EXPORTS = ("odp_grid_create", "odp_grid_destroy", "odp_grid_info", "odp_hj_solve", "odp_hj_solve_host",
+           "odp_last_launch_count", "odp_last_error", "odp_version")
+
+
+class odp_solve_opts(ctypes.Structure):
+    _fields_ = [("cfl", ctypes.c_double),
+                ("target", ctypes.c_void_p),
+                ("stream", ctypes.c_void_p),
+                ("write_initial", ctypes.c_int),
+                ("kernel", ctypes.c_int),
+                ("use_graph", ctypes.c_int),
+                ("tau_reached", ctypes.POINTER(ctypes.c_double)),
+                ("steps_taken", ctypes.POINTER(ctypes.c_longlong)),
+                ("stages_taken", ctypes.POINTER(ctypes.c_longlong)),
+                ("kernel_ms", ctypes.POINTER(ctypes.c_double))]
+
+
+class OdpError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"odp status {status}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2204_05520_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    D = ctypes.POINTER(ctypes.c_double)
+    I64 = ctypes.POINTER(ctypes.c_int64)
+    vp = ctypes.c_void_p
+    lib.odp_grid_create.argtypes = [ctypes.c_int, D, D, I64, ctypes.c_uint32, ctypes.POINTER(vp)]
+    lib.odp_grid_create.restype = ctypes.c_int
+    lib.odp_grid_destroy.argtypes = [vp]
+    lib.odp_grid_destroy.restype = None
+    lib.odp_grid_info.argtypes = [vp, ctypes.POINTER(ctypes.c_int), I64, D, I64]
+    lib.odp_grid_info.restype = ctypes.c_int
+    for name in ("odp_hj_solve", "odp_hj_solve_host"):
+        f = getattr(lib, name)
+        f.argtypes = [vp, ctypes.c_int, D, ctypes.c_int, vp, D, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp,
+                      ctypes.POINTER(odp_solve_opts)]
+        f.restype = ctypes.c_int
+    lib.odp_last_launch_count.argtypes = [vp]
+    lib.odp_last_launch_count.restype = ctypes.c_longlong
+    lib.odp_last_error.argtypes = []
+    lib.odp_last_error.restype = ctypes.c_char_p
+    lib.odp_version.argtypes = []
+    lib.odp_version.restype = ctypes.c_char_p
+    return lib
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def last_error() -> str:
+    return _lib.odp_last_error().decode()
+
+
+def version() -> str:
+    return _lib.odp_version().decode()
+
+
+def _check(status: int):
+    if status != ODP_OK:
+        raise OdpError(status, last_error())
+
+
+def _dp(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+class Grid:
+    """odp_grid_create / odp_grid_destroy."""
+
+    def __init__(self, N: Sequence[int], lo: Sequence[float], hi: Sequence[float], periodic_mask: int = 0):
+        self.N = tuple(int(v) for v in N)
+        Na = np.ascontiguousarray(self.N, dtype=np.int64)
+        loa, lop = _dp(lo)
+        hia, hip = _dp(hi)
+        h = ctypes.c_void_p()
+        _check(_lib.odp_grid_create(len(self.N), lop, hip, Na.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                    ctypes.c_uint32(periodic_mask), ctypes.byref(h)))
+        self.handle = h
+
+    @property
+    def points(self) -> int:
+        return int(np.prod(self.N, dtype=np.int64))
+
+    def info(self):
+        dims = ctypes.c_int()
+        N = np.zeros(6, dtype=np.int64)
+        dx = np.zeros(6)
+        P = ctypes.c_int64()
+        _check(_lib.odp_grid_info(self.handle, ctypes.byref(dims), N.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                  dx.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(P)))
+        n = dims.value
+        return dict(dims=n, N=tuple(N[:n]), dx=tuple(dx[:n]), points=P.value)
+
+    def launch_count(self) -> int:
+        return int(_lib.odp_last_launch_count(self.handle))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.odp_grid_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class SolveInfo(dict):
+    pass
+
+
+def _opts(cfl, target_ptr, stream_ptr, write_initial, kernel, timing):
+    o = odp_solve_opts()
+    o.cfl = float(cfl or 0.0)
+    o.target = target_ptr
+    o.stream = stream_ptr
+    o.write_initial = int(bool(write_initial))
+    o.kernel = KERNEL[kernel]
+    o.use_graph = 0
+    tr = ctypes.c_double()
+    st = ctypes.c_longlong()
+    sg = ctypes.c_longlong()
+    km = (ctypes.c_double * 3)()
+    o.tau_reached = ctypes.pointer(tr)
+    o.steps_taken = ctypes.pointer(st)
+    o.stages_taken = ctypes.pointer(sg)
+    o.kernel_ms = ctypes.cast(km, ctypes.POINTER(ctypes.c_double)) if timing else None
+    return o, (tr, st, sg, km)
+
+
+def _info(keep, timing, status):
+    tr, st, sg, km = keep
+    info = SolveInfo(tau_reached=tr.value, steps=st.value, stages=sg.value, status=status)
+    if timing:
+        info["kernel_ms"] = dict(pass1=km[0], pass2=km[1], control=km[2])
+    return info
+
+
+def hj_solve(grid: Grid, dynamics: str, params, V0, tau, accuracy: str, mode: str, out=None, cfl: float = 0.0,
+             target=None, write_initial: bool = False, kernel: str = "auto", stream=None, timing: bool = False,
+             raise_on_error: bool = True):
+    """odp_hj_solve on torch CUDA tensors (device pointers).  Returns (out, info)."""
+    import torch
+    assert V0.is_cuda and V0.dtype == torch.float32 and V0.is_contiguous()
+    ntau = len(tau)
+    nout = ntau if write_initial else ntau - 1
+    if out is None:
+        out = torch.empty((nout,) + tuple(grid.N), dtype=torch.float32, device=V0.device)
+    assert out.is_cuda and out.dtype == torch.float32 and out.is_contiguous() and out.numel() == nout * grid.points
+    if target is not None:
+        assert target.is_cuda and target.dtype == torch.float32 and target.is_contiguous()
+    if stream is None:
+        stream = torch.cuda.current_stream(V0.device)
+    pa, pp = _dp(params)
+    ta, tp = _dp(tau)
+    o, keep = _opts(cfl, target.data_ptr() if target is not None else None, stream.cuda_stream, write_initial,
+                    kernel, timing)
+    status = _lib.odp_hj_solve(grid.handle, DYNAMICS[dynamics], pp, len(pa), V0.data_ptr(), tp, len(ta),
+                               ACCURACY[accuracy], MODE[mode], out.data_ptr(), ctypes.byref(o))
+    if status != ODP_OK and raise_on_error:
+        raise OdpError(status, last_error())
+    return out, _info(keep, timing, status)
+
+
+def hj_solve_host(grid: Grid, dynamics: str, params, V0: np.ndarray, tau, accuracy: str, mode: str, out=None,
+                  cfl: float = 0.0, target=None, write_initial: bool = False, kernel: str = "auto", stream=None,
+                  timing: bool = False, raise_on_error: bool = True):
+    """odp_hj_solve_host: V0/out/target are host arrays (numpy or pinned torch CPU tensors)."""
+    def host_ptr(a):
+        if hasattr(a, "data_ptr"):
+            return a.data_ptr()
+        assert a.dtype == np.float32 and a.flags["C_CONTIGUOUS"]
+        return a.ctypes.data
+    ntau = len(tau)
+    nout = ntau if write_initial else ntau - 1
+    if out is None:
+        out = np.empty((nout,) + tuple(grid.N), dtype=np.float32)
+    pa, pp = _dp(params)
+    ta, tp = _dp(tau)
+    o, keep = _opts(cfl, host_ptr(target) if target is not None else None,
+                    stream.cuda_stream if stream is not None else None, write_initial, kernel, timing)
+    status = _lib.odp_hj_solve_host(grid.handle, DYNAMICS[dynamics], pp, len(pa), host_ptr(V0), tp, len(ta),
+                                    ACCURACY[accuracy], MODE[mode], host_ptr(out), ctypes.byref(o))
+    if status != ODP_OK and raise_on_error:
+        raise OdpError(status, last_error())
+    return out, _info(keep, timing, status)

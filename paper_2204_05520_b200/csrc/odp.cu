@@ -1,0 +1,626 @@
+// odp.cu -- C-ABI (include/odp.h), host orchestrator and kernel instantiation of the B200 HJ
+// level-set step.  One translation unit: libodp.so.
+//
+// Host orchestration of Algorithm 2 per save interval (reading A9):
+//   begin(tau_k) -> chunks of steps [pass1 -> finalize -> pass2 (-> pass1 -> finalize -> pass2)
+//   -> advance] launched back to back; every kernel early-exits once the device state says the
+//   interval is done, so the host polls the 80-byte state only between chunks.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/odp.h"
+#include "kernels_stream.cuh"
+
+using namespace odp;
+
+// ------------------------------------------------------------------------------------------------
+// errors
+// ------------------------------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static odp_status fail(odp_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define CUDA_TRY(expr)                                                                            \
+    do {                                                                                          \
+        cudaError_t e_ = (expr);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            return fail(e_ == cudaErrorMemoryAllocation ? ODP_ENOMEM : ODP_ECUDA, "%s: %s (%s:%d)", \
+                        #expr, cudaGetErrorString(e_), __FILE__, __LINE__);                       \
+    } while (0)
+
+// ------------------------------------------------------------------------------------------------
+// finalize / time-loop control kernels (Alg. 2 l.164-167; readings A7, A9, A19, A20)
+// ------------------------------------------------------------------------------------------------
+template <class F, int NDIM>
+__global__ void __launch_bounds__(256) k_finalize(const float *__restrict__ partials, int nparts, DevState *st,
+                                                  GridDev g, FParams fp, const double *__restrict__ dxd,
+                                                  int stage_in_step, int final_check) {
+    if (!st->active) return;
+    constexpr int Q = 2 * NDIM + 2;
+    __shared__ float red[Q][8];
+    __shared__ float rng[Q];
+    __shared__ int bad;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // reduce the per-CTA partials of pass 1 (min/max are exact: any order gives the same bits)
+    for (int q = 0; q < Q; ++q) {
+        float r = q < NDIM ? __int_as_float(0x7f800000) : (q < 2 * NDIM ? -__int_as_float(0x7f800000) : 0.f);
+        for (int p = threadIdx.x; p < nparts; p += blockDim.x) {
+            const float o = partials[(long long)p * Q + q];
+            r = q < NDIM ? fminf(r, o) : fmaxf(r, o);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const float o = __shfl_xor_sync(0xffffffffu, r, off);
+            r = q < NDIM ? fminf(r, o) : fmaxf(r, o);
+        }
+        if (lane == 0) red[q][warp] = r;
+    }
+    __syncthreads();
+    if (threadIdx.x < Q) {
+        const int q = threadIdx.x;
+        float r = red[q][0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = q < NDIM ? fminf(r, red[q][w]) : fmaxf(r, red[q][w]);
+        rng[q] = r;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int d = 0; d < NDIM; ++d) { st->minD[d] = rng[d]; st->maxD[d] = rng[NDIM + d]; }
+        st->maxabs = rng[2 * NDIM];
+        st->nan = rng[2 * NDIM + 1] != 0.f;
+        bad = st->nan || !(rng[2 * NDIM] <= 1e10f);
+        if (bad) { st->status = ODP_ENUMERIC; st->active = 0; }
+        else if (final_check) st->active = 0;
+        else st->stages += 1;
+    }
+    __syncthreads();
+    if (bad || final_check || stage_in_step != 0) return;
+
+    // alpha^max_d = max over the nodes of alpha_{i,d}: enumerate the (<= 2) coordinate axes that
+    // alpha_d depends on (functor deps); any other coordinate is irrelevant to alpha_d.
+    F f;
+    f.init(fp, rng, rng + NDIM);
+    __shared__ float am[NDIM];
+    for (int d = 0; d < NDIM; ++d) {
+        const int m = F::deps(d);
+        int ax[2] = {-1, -1}, na = 0;
+        for (int a = 0; a < NDIM; ++a) if ((m >> a) & 1) ax[na++] = a;
+        const int n0 = na > 0 ? g.Ng[ax[0]] : 1, n1 = na > 1 ? g.Ng[ax[1]] : 1;
+        float r = 0.f;
+        for (int t = threadIdx.x; t < n0 * n1; t += blockDim.x) {
+            Pt q;
+            if (na > 0) load_axis<F>(g, q, ax[0], t % n0);
+            if (na > 1) load_axis<F>(g, q, ax[1], t / n0);
+            r = fmaxf(r, f.alpha(d, q));
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) r = fmaxf(r, __shfl_xor_sync(0xffffffffu, r, off));
+        if (lane == 0) red[0][warp] = r;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float a = red[0][0];
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) a = fmaxf(a, red[0][w]);
+            am[d] = a;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double sum = 0.0;                                             // Alg. 2 l.167
+        for (int d = 0; d < NDIM; ++d) { st->amax[d] = am[d]; sum += fabs((double)am[d]) / dxd[d]; }
+        const double rem = st->tau_target - st->tau;
+        double dt = sum > 0.0 ? st->cfl / sum : rem;                 // A20
+        if (dt > rem) dt = rem;                                       // A9
+        st->dt = dt;
+        st->dt_f = (float)dt;
+    }
+}
+
+__global__ void k_init_state(DevState *st, double cfl, double eps) {
+    st->tau = 0.0; st->tau_target = 0.0; st->eps = eps; st->dt = 0.0; st->cfl = cfl; st->dt_f = 0.f;
+    st->maxabs = 0.f; st->nan = 0; st->active = 0; st->status = 0; st->steps = 0; st->stages = 0;
+    for (int d = 0; d < MAXD; ++d) { st->minD[d] = 0.f; st->maxD[d] = 0.f; st->amax[d] = 0.f; }
+}
+
+__global__ void k_begin(DevState *st, double tau_k) {
+    st->tau_target = tau_k;
+    st->active = (st->status == 0 && tau_k - st->tau > st->eps) ? 1 : 0;
+}
+
+__global__ void k_force_active(DevState *st) { st->active = st->status == 0 ? 1 : 0; }
+
+__global__ void k_advance(DevState *st) {                               // O8: tau += dt (float64)
+    if (!st->active) return;
+    st->tau += st->dt;
+    st->steps += 1;
+    if (st->tau_target - st->tau <= st->eps) st->active = 0;
+}
+
+// ------------------------------------------------------------------------------------------------
+// kernel tables
+// ------------------------------------------------------------------------------------------------
+typedef void (*pass1_fn)(GridDev, const float *, float *, const DevState *);
+typedef void (*pass2_fn)(GridDev, const float *, const float *, const float *, float *, const DevState *, FParams,
+                         int, int);
+typedef void (*fin_fn)(const float *, int, DevState *, GridDev, FParams, const double *, int, int);
+
+struct KernelSet {
+    pass1_fn pass1 = nullptr;
+    pass2_fn pass2 = nullptr;
+    fin_fn fin = nullptr;
+    TiledFns tiled;      // tiled family (may be empty)
+    StreamFnsAll stream; // stream family (may be empty)
+};
+
+template <class F, int NDIM, int R>
+static KernelSet make_set() {
+    KernelSet k;
+    k.pass1 = k_pass1_generic<NDIM, R>;
+    k.pass2 = k_pass2_generic<F, NDIM, R>;
+    k.fin = k_finalize<F, NDIM>;
+    k.tiled = tiled_fns<F, NDIM, R>();
+    k.stream = stream_fns<F, NDIM, R>();
+    return k;
+}
+
+template <template <int> class FH, int R>
+static KernelSet holo_set(int n) {
+    switch (n) {
+    case 1: return make_set<FH<1>, 1, R>();
+    case 2: return make_set<FH<2>, 2, R>();
+    case 3: return make_set<FH<3>, 3, R>();
+    case 4: return make_set<FH<4>, 4, R>();
+    case 5: return make_set<FH<5>, 5, R>();
+    default: return make_set<FH<6>, 6, R>();
+    }
+}
+
+template <int R>
+static KernelSet select_set_r(int dyn, int n) {
+    switch (dyn) {
+    case ODP_DYN_HOLONOMIC_BALL: return holo_set<FHoloBall, R>(n);
+    case ODP_DYN_HOLONOMIC_BOX: return holo_set<FHoloBox, R>(n);
+    case ODP_DYN_DUBINS3D: return make_set<FDubins3D, 3, R>();
+    case ODP_DYN_CAR4D: return make_set<FCar4D, 4, R>();
+    case ODP_DYN_CAR5D: return make_set<FCar5D, 5, R>();
+    default: return make_set<FDoubleInt6D, 6, R>();
+    }
+}
+
+static KernelSet select_set(int dyn, int n, int R) { return R == 1 ? select_set_r<1>(dyn, n) : select_set_r<2>(dyn, n); }
+
+// ------------------------------------------------------------------------------------------------
+// grid handle
+// ------------------------------------------------------------------------------------------------
+struct odp_grid {
+    int n = 0;
+    int64_t N[MAXD] = {0};
+    double lo[MAXD] = {0}, hi[MAXD] = {0}, dx[MAXD] = {0};
+    int per[MAXD] = {0};
+    int64_t P = 0;
+    // device cache (allocated lazily on the device current at the first solve)
+    int device = -1;
+    float *d_tab = nullptr;
+    int tab_off[MAXD] = {0};
+    double *d_dx = nullptr;
+    float *d_buf[2] = {nullptr, nullptr};
+    size_t buf_elems = 0;
+    int64_t halo_elems = 0;       // R_MAX planes before local plane 0
+    float *d_partials = nullptr;
+    int max_parts = 0;
+    DevState *d_state = nullptr;
+    DevState *h_state = nullptr;  // pinned
+    cudaStream_t own_stream = nullptr;
+    std::vector<cudaEvent_t> events;
+    long long launches = 0;
+};
+
+static constexpr int R_MAX = 2;
+
+static void free_device(odp_grid *g) {
+    if (g->device < 0) return;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    cudaSetDevice(g->device);
+    cudaFree(g->d_tab); cudaFree(g->d_dx);
+    cudaFree(g->d_buf[0]); cudaFree(g->d_buf[1]);
+    cudaFree(g->d_partials); cudaFree(g->d_state);
+    if (g->h_state) cudaFreeHost(g->h_state);
+    if (g->own_stream) cudaStreamDestroy(g->own_stream);
+    for (auto e : g->events) cudaEventDestroy(e);
+    g->events.clear();
+    g->d_tab = nullptr; g->d_dx = nullptr; g->d_buf[0] = g->d_buf[1] = nullptr; g->d_partials = nullptr;
+    g->d_state = nullptr; g->h_state = nullptr; g->own_stream = nullptr;
+    g->device = -1;
+    if (cur >= 0) cudaSetDevice(cur);
+}
+
+extern "C" odp_status odp_grid_create(int dims, const double *lo, const double *hi, const int64_t *N,
+                                      uint32_t periodic_mask, odp_grid **out) {
+    g_err.clear();
+    if (!out) return fail(ODP_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (dims < 1 || dims > MAXD) return fail(ODP_EINVAL, "dims=%d not in 1..6", dims);
+    if (!lo || !hi || !N) return fail(ODP_EINVAL, "NULL lo/hi/N");
+    odp_grid *g = new (std::nothrow) odp_grid();
+    if (!g) return fail(ODP_ENOMEM, "host allocation");
+    g->n = dims;
+    g->P = 1;
+    for (int d = 0; d < dims; ++d) {
+        if (N[d] < 3) { delete g; return fail(ODP_EINVAL, "N[%d]=%lld < 3", d, (long long)N[d]); }
+        if (!(lo[d] < hi[d])) { delete g; return fail(ODP_EINVAL, "lo[%d] >= hi[%d]", d, d); }
+        if (N[d] > (int64_t)1 << 30) { delete g; return fail(ODP_EINVAL, "N[%d] too large", d); }
+        g->N[d] = N[d]; g->lo[d] = lo[d]; g->hi[d] = hi[d];
+        g->per[d] = (periodic_mask >> d) & 1u;
+        g->dx[d] = g->per[d] ? (hi[d] - lo[d]) / (double)N[d] : (hi[d] - lo[d]) / (double)(N[d] - 1);   // A15
+        g->P *= N[d];
+    }
+    if (dims > 1 && g->P / g->N[0] > ((int64_t)1 << 31) - 1) { delete g; return fail(ODP_EINVAL, "axis-0 plane exceeds 2^31 points"); }
+    *out = g;
+    return ODP_OK;
+}
+
+extern "C" void odp_grid_destroy(odp_grid *g) {
+    if (!g) return;
+    free_device(g);
+    delete g;
+}
+
+extern "C" odp_status odp_grid_info(const odp_grid *g, int *dims, int64_t *N, double *dx, int64_t *points) {
+    g_err.clear();
+    if (!g) return fail(ODP_EINVAL, "NULL grid");
+    if (dims) *dims = g->n;
+    for (int d = 0; d < g->n; ++d) {
+        if (N) N[d] = g->N[d];
+        if (dx) dx[d] = g->dx[d];
+    }
+    if (points) *points = g->P;
+    return ODP_OK;
+}
+
+extern "C" long long odp_last_launch_count(const odp_grid *g) { return g ? g->launches : 0; }
+extern "C" const char *odp_last_error(void) { return g_err.c_str(); }
+extern "C" const char *odp_version(void) { return "odp-b200 0.1 sm_100a"; }
+
+static odp_status ensure_device(odp_grid *g, int nparts_needed) {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    if (g->device >= 0 && g->device != dev) free_device(g);
+    const int64_t plane = g->P / g->N[0];
+    if (g->device < 0) {
+        g->device = dev;
+        // coordinate tables x, cos x, sin x per axis: float64 host values rounded to float32 (A26)
+        std::vector<float> tab;
+        for (int d = 0; d < g->n; ++d) {
+            g->tab_off[d] = (int)tab.size();
+            for (int k = 0; k < 3; ++k)
+                for (int64_t i = 0; i < g->N[d]; ++i) {
+                    const double x = g->lo[d] + (double)i * g->dx[d];
+                    tab.push_back((float)(k == 0 ? x : (k == 1 ? std::cos(x) : std::sin(x))));
+                }
+        }
+        CUDA_TRY(cudaMalloc(&g->d_tab, tab.size() * sizeof(float)));
+        CUDA_TRY(cudaMemcpy(g->d_tab, tab.data(), tab.size() * sizeof(float), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMalloc(&g->d_dx, MAXD * sizeof(double)));
+        CUDA_TRY(cudaMemcpy(g->d_dx, g->dx, MAXD * sizeof(double), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMalloc(&g->d_state, sizeof(DevState)));
+        CUDA_TRY(cudaMallocHost(&g->h_state, sizeof(DevState)));
+        CUDA_TRY(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
+    }
+    if (!g->d_buf[0]) {
+        g->halo_elems = R_MAX * plane;
+        g->buf_elems = (size_t)(g->P + 2 * g->halo_elems);
+        for (int b = 0; b < 2; ++b) {
+            CUDA_TRY(cudaMalloc(&g->d_buf[b], g->buf_elems * sizeof(float)));
+            CUDA_TRY(cudaMemset(g->d_buf[b], 0, g->buf_elems * sizeof(float)));
+        }
+    }
+    if (g->max_parts < nparts_needed) {
+        cudaFree(g->d_partials);
+        g->d_partials = nullptr;
+        CUDA_TRY(cudaMalloc(&g->d_partials, (size_t)nparts_needed * (2 * MAXD + 2) * sizeof(float)));
+        g->max_parts = nparts_needed;
+    }
+    return ODP_OK;
+}
+
+static GridDev make_griddev(const odp_grid *g) {
+    GridDev d;
+    memset(&d, 0, sizeof d);
+    d.n = g->n;
+    for (int k = 0; k < g->n; ++k) {
+        d.N[k] = (int)g->N[k];
+        d.Ng[k] = (int)g->N[k];
+        d.per[k] = g->per[k];
+        d.inv_dx[k] = (float)(1.0 / g->dx[k]);
+        d.dx[k] = (float)g->dx[k];
+        d.tab_off[k] = g->tab_off[k];
+    }
+    d.stride[g->n - 1] = 1;
+    for (int k = g->n - 2; k >= 0; --k) d.stride[k] = d.stride[k + 1] * g->N[k + 1];
+    d.P = g->P;
+    d.Ng0 = (int)g->N[0];
+    d.g0 = 0;
+    d.tab = g->d_tab;
+    return d;
+}
+
+static const int kWantParams[6] = {2, 3, 3, 5, 3, 3};
+static const int kWantDims[6] = {0, 0, 3, 4, 5, 6};
+
+static odp_status validate(const odp_grid *g, int dyn, const double *params, int nparams, const double *tau,
+                           int ntau, int accuracy, int mode) {
+    if (!g) return fail(ODP_EINVAL, "NULL grid");
+    if (dyn < 0 || dyn > 5) return fail(ODP_EINVAL, "unknown dynamics id %d", dyn);
+    if (!params || nparams != kWantParams[dyn]) return fail(ODP_EINVAL, "dynamics %d takes %d params (got %d)", dyn, kWantParams[dyn], nparams);
+    if (kWantDims[dyn] && kWantDims[dyn] != g->n) return fail(ODP_EINVAL, "dynamics %d needs dims=%d (grid has %d)", dyn, kWantDims[dyn], g->n);
+    const double goal = params[nparams - 1];
+    if (goal != 1.0 && goal != -1.0) return fail(ODP_EINVAL, "goal must be -1 or +1");
+    for (int k = 0; k < nparams; ++k) if (!std::isfinite(params[k])) return fail(ODP_EINVAL, "param %d not finite", k);
+    if (accuracy != ODP_LOW && accuracy != ODP_MEDIUM) return fail(ODP_EINVAL, "accuracy %d", accuracy);
+    if (mode != ODP_BRS && mode != ODP_BRT) return fail(ODP_EINVAL, "mode %d", mode);
+    if (!tau || ntau < 2) return fail(ODP_EINVAL, "need ntau >= 2");
+    if (tau[0] != 0.0) return fail(ODP_EINVAL, "tau[0] must be 0");
+    for (int k = 1; k < ntau; ++k) if (!(tau[k] > tau[k - 1])) return fail(ODP_EINVAL, "tau not strictly increasing at %d", k);
+    return ODP_OK;
+}
+
+namespace {
+struct Launch {
+    int kind;          // 0 pass1, 1 pass2, 2 finalize/control
+    int ev;            // index of the start event (stop = ev + 1), -1 if untimed
+};
+}
+
+static odp_status solve_device(odp_grid *g, int dyn, const double *params, int nparams, const float *V0,
+                               const double *tau, int ntau, int accuracy, int mode, float *out,
+                               const odp_solve_opts *opts) {
+    odp_status st = validate(g, dyn, params, nparams, tau, ntau, accuracy, mode);
+    if (st) return st;
+    if (!V0 || !out) return fail(ODP_EINVAL, "NULL V0/out");
+    const int R = accuracy == ODP_LOW ? 1 : 2;
+    const int n = g->n;
+    KernelSet ks = select_set(dyn, n, R);
+
+    const int want_kernel = opts ? opts->kernel : ODP_KERNEL_AUTO;
+    GridDev gd_probe;
+    memset(&gd_probe, 0, sizeof gd_probe);
+
+    // launch geometry of the generic family
+    const int block = 256;
+    int nsm = 148;
+    {
+        int dev = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    long long want_blocks = (g->P + block - 1) / block;
+    int grid_generic = (int)std::min<long long>(want_blocks, (long long)nsm * 8);
+
+    if ((st = ensure_device(g, std::max(grid_generic, nsm * 8)))) return st;
+    GridDev gd = make_griddev(g);
+
+    bool use_stream = false, use_tiled = false;
+    StreamPlan sp;
+    StreamFns sfn;
+    TiledPlan tp;
+    if (want_kernel == ODP_KERNEL_AUTO || want_kernel == ODP_KERNEL_STREAM)
+        use_stream = stream_plan(gd, R, ks.stream, &sfn, &sp);
+    if (want_kernel == ODP_KERNEL_STREAM && !use_stream) return fail(ODP_EINVAL, "stream kernels do not cover this grid");
+    if (!use_stream && (want_kernel == ODP_KERNEL_AUTO || want_kernel == ODP_KERNEL_TILED) && ks.tiled.pass1)
+        use_tiled = tiled_plan(gd, R, nsm, &tp);
+    if (want_kernel == ODP_KERNEL_TILED && !use_tiled) return fail(ODP_EINVAL, "tiled kernels do not cover this grid");
+    if (use_stream) {
+        if (stream_prepare(sfn, sp, nsm)) return fail(ODP_ECUDA, "stream kernel attribute setup failed");
+        if ((st = ensure_device(g, sp.grid))) return st;
+    }
+    if (use_tiled) {
+        if (tiled_prepare(ks.tiled, tp, nsm)) return fail(ODP_ECUDA, "tiled kernel attribute setup failed");
+        if ((st = ensure_device(g, tp.grid))) return st;
+    }
+    const int nparts = use_stream ? sp.grid : (use_tiled ? tp.grid : grid_generic);
+
+    cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
+    const double cfl = (opts && opts->cfl > 0.0) ? opts->cfl : (accuracy == ODP_LOW ? 0.8 : 0.5);   // A7
+    const double eps = 1e-12 * std::max(1.0, tau[ntau - 1]);
+    const int brt = mode == ODP_BRT;
+    const float *T = (opts && opts->target) ? opts->target : V0;
+    const int write_initial = opts ? opts->write_initial : 0;
+    const bool timed = opts && opts->kernel_ms;
+    double kms[3] = {0, 0, 0};
+
+    FParams fp;
+    memset(&fp, 0, sizeof fp);
+    for (int k = 0; k < nparams; ++k) fp.c[k] = (float)params[k];
+
+    float *buf[2] = {g->d_buf[0] + g->halo_elems, g->d_buf[1] + g->halo_elems};
+    const size_t bytes = (size_t)g->P * sizeof(float);
+    g->launches = 0;
+
+    CUDA_TRY(cudaMemcpyAsync(buf[0], V0, bytes, cudaMemcpyDeviceToDevice, s));
+    k_init_state<<<1, 1, 0, s>>>(g->d_state, cfl, eps);
+    ++g->launches;
+    CUDA_TRY(cudaGetLastError());
+    int k_out = 0;
+    if (write_initial) {
+        CUDA_TRY(cudaMemcpyAsync(out, V0, bytes, cudaMemcpyDeviceToDevice, s));
+        k_out = 1;
+    }
+
+    std::vector<Launch> launches;
+    auto ensure_events = [&](size_t nev) -> odp_status {
+        while (g->events.size() < nev) {
+            cudaEvent_t e;
+            CUDA_TRY(cudaEventCreate(&e));
+            g->events.push_back(e);
+        }
+        return ODP_OK;
+    };
+
+    auto launch_pass1 = [&](const float *W) {
+        if (use_stream) stream_pass1(sfn, sp, gd, W, g->d_partials, g->d_state, s);
+        else if (use_tiled) tiled_pass1(ks.tiled, tp, gd, W, g->d_partials, g->d_state, s);
+        else ks.pass1<<<grid_generic, block, 0, s>>>(gd, W, g->d_partials, g->d_state);
+    };
+    auto launch_pass2 = [&](const float *W, const float *Vn, float *o, int kind) {
+        if (use_stream) stream_pass2(sfn, sp, gd, W, Vn, T, o, g->d_state, fp, kind, brt, s);
+        else if (use_tiled) tiled_pass2(ks.tiled, tp, gd, W, Vn, T, o, g->d_state, fp, kind, brt, s);
+        else ks.pass2<<<grid_generic, block, 0, s>>>(gd, W, Vn, T, o, g->d_state, fp, kind, brt);
+    };
+    auto launch_fin = [&](int stage_in_step, int final_check) {
+        ks.fin<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, gd, fp, g->d_dx, stage_in_step, final_check);
+    };
+
+    // one timed/untimed launch wrapper; events are recorded only when kernel times are requested
+    int ev_next = 0;
+    auto rec = [&](int kind, auto &&fn) -> odp_status {
+        int ev = -1;
+        if (timed) {
+            odp_status e = ensure_events((size_t)ev_next + 2);
+            if (e) return e;
+            ev = ev_next;
+            ev_next += 2;
+            CUDA_TRY(cudaEventRecord(g->events[ev], s));
+        }
+        fn();
+        ++g->launches;
+        if (timed) CUDA_TRY(cudaEventRecord(g->events[ev + 1], s));
+        launches.push_back({kind, ev});
+        return ODP_OK;
+    };
+
+    int cur = 0;                       // index of the buffer holding the current V
+    odp_status rs = ODP_OK;
+    for (int k = 1; k < ntau && rs == ODP_OK; ++k) {
+        k_begin<<<1, 1, 0, s>>>(g->d_state, tau[k]);
+        ++g->launches;
+        CUDA_TRY(cudaMemcpyAsync(g->h_state, g->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        long long s0 = g->h_state->steps;
+        int chunk = 2;
+        std::vector<int> step_of_launch;
+        while (g->h_state->active) {
+            launches.clear();
+            step_of_launch.clear();
+            ev_next = 0;
+            for (int j = 0; j < chunk; ++j) {
+                const int a = (cur + j) & 1, b = a ^ 1;
+                if (accuracy == ODP_LOW) {
+                    if ((rs = rec(0, [&] { launch_pass1(buf[a]); }))) return rs;
+                    if ((rs = rec(2, [&] { launch_fin(0, 0); }))) return rs;
+                    if ((rs = rec(1, [&] { launch_pass2(buf[a], nullptr, buf[b], STAGE_EULER); }))) return rs;
+                } else {
+                    if ((rs = rec(0, [&] { launch_pass1(buf[0]); }))) return rs;
+                    if ((rs = rec(2, [&] { launch_fin(0, 0); }))) return rs;
+                    if ((rs = rec(1, [&] { launch_pass2(buf[0], nullptr, buf[1], STAGE_RK1); }))) return rs;
+                    if ((rs = rec(0, [&] { launch_pass1(buf[1]); }))) return rs;
+                    if ((rs = rec(2, [&] { launch_fin(1, 0); }))) return rs;
+                    if ((rs = rec(1, [&] { launch_pass2(buf[1], buf[0], buf[0], STAGE_RK2); }))) return rs;
+                }
+                if ((rs = rec(2, [&] { k_advance<<<1, 1, 0, s>>>(g->d_state); }))) return rs;
+                while (step_of_launch.size() < launches.size()) step_of_launch.push_back(j);
+            }
+            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(cudaMemcpyAsync(g->h_state, g->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            const long long done = g->h_state->steps - s0;
+            s0 = g->h_state->steps;
+            if (accuracy == ODP_LOW && (done & 1)) cur ^= 1;
+            if (timed) {
+                for (size_t q = 0; q < launches.size(); ++q) {
+                    if (step_of_launch[q] >= done) continue;      // launches that found the interval done
+                    float ms = 0.f;
+                    CUDA_TRY(cudaEventElapsedTime(&ms, g->events[launches[q].ev], g->events[launches[q].ev + 1]));
+                    kms[launches[q].kind] += ms;
+                }
+            }
+            if (g->h_state->status) { rs = ODP_ENUMERIC; break; }
+            // size the next chunk from the remaining time and the current dt (+1 for the clipped step)
+            const double rem = g->h_state->tau_target - g->h_state->tau;
+            const long long est = g->h_state->dt > 0 ? (long long)std::ceil(rem / g->h_state->dt) + 1 : 2;
+            chunk = (int)std::max<long long>(1, std::min<long long>(est, 256));
+        }
+        if (rs != ODP_OK) break;
+        CUDA_TRY(cudaMemcpyAsync(out + (size_t)k_out * g->P, buf[accuracy == ODP_LOW ? cur : 0], bytes,
+                                 cudaMemcpyDeviceToDevice, s));
+        ++k_out;
+    }
+    if (rs == ODP_OK) {
+        // final guard on the last V (reading A19)
+        const float *Wf = buf[accuracy == ODP_LOW ? cur : 0];
+        k_force_active<<<1, 1, 0, s>>>(g->d_state);
+        launch_pass1(Wf);
+        launch_fin(0, 1);
+        g->launches += 3;
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(g->h_state, g->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (g->h_state->status) rs = ODP_ENUMERIC;
+    }
+    if (opts) {
+        if (opts->tau_reached) *opts->tau_reached = g->h_state->tau;
+        if (opts->steps_taken) *opts->steps_taken = g->h_state->steps;
+        if (opts->stages_taken) *opts->stages_taken = g->h_state->stages;
+        if (opts->kernel_ms) for (int q = 0; q < 3; ++q) opts->kernel_ms[q] = kms[q];
+    }
+    if (rs == ODP_ENUMERIC)
+        return fail(ODP_ENUMERIC, "numerical failure (NaN or |V| > 1e10) at tau = %.9g", g->h_state->tau);
+    return rs;
+}
+
+extern "C" odp_status odp_hj_solve(odp_grid *g, int dynamics_id, const double *params, int nparams, const float *V0,
+                                   const double *tau, int ntau, int accuracy, int mode, float *out,
+                                   const odp_solve_opts *opts) {
+    g_err.clear();
+    return solve_device(g, dynamics_id, params, nparams, V0, tau, ntau, accuracy, mode, out, opts);
+}
+
+extern "C" odp_status odp_hj_solve_host(odp_grid *g, int dynamics_id, const double *params, int nparams,
+                                        const float *V0, const double *tau, int ntau, int accuracy, int mode,
+                                        float *out, const odp_solve_opts *opts) {
+    g_err.clear();
+    odp_status st = validate(g, dynamics_id, params, nparams, tau, ntau, accuracy, mode);
+    if (st) return st;
+    if (!V0 || !out) return fail(ODP_EINVAL, "NULL V0/out");
+    if ((st = ensure_device(g, 1))) return st;
+    const int nout = (opts && opts->write_initial) ? ntau : ntau - 1;
+    const size_t bytes = (size_t)g->P * sizeof(float);
+    cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
+    float *dV0 = nullptr, *dout = nullptr, *dT = nullptr;
+    CUDA_TRY(cudaMallocAsync(&dV0, bytes, s));
+    CUDA_TRY(cudaMallocAsync(&dout, bytes * nout, s));
+    odp_solve_opts o;
+    memset(&o, 0, sizeof o);
+    if (opts) o = *opts;
+    o.stream = s;
+    if (opts && opts->target) {
+        CUDA_TRY(cudaMallocAsync(&dT, bytes, s));
+        CUDA_TRY(cudaMemcpyAsync(dT, opts->target, bytes, cudaMemcpyHostToDevice, s));
+        o.target = dT;
+    }
+    CUDA_TRY(cudaMemcpyAsync(dV0, V0, bytes, cudaMemcpyHostToDevice, s));
+    st = solve_device(g, dynamics_id, params, nparams, dV0, tau, ntau, accuracy, mode, dout, &o);
+    if (st == ODP_OK || st == ODP_ENUMERIC) {
+        cudaError_t e = cudaMemcpyAsync(out, dout, bytes * nout, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess && st == ODP_OK) st = fail(ODP_ECUDA, "copy out: %s", cudaGetErrorString(e));
+    }
+    cudaFreeAsync(dV0, s);
+    cudaFreeAsync(dout, s);
+    if (dT) cudaFreeAsync(dT, s);
+    cudaStreamSynchronize(s);
+    return st;
+}

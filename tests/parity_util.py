@@ -1,0 +1,80 @@
+"""Shared helpers of the GPU parity tests: run a workload through the C-ABI and through the oracle,
+compare element by element."""
+import numpy as np
+
+TOL = 1e-4     # north_star: max |V_gpu - V_oracle| <= 1e-4 (float32)
+BAND = 1e-4    # membership (V <= 0) identical outside |V_oracle| < 1e-4 (reading A24)
+
+
+def run_gpu(w, V0, kernel="auto", **kw):
+    import torch
+    import paper_2204_05520_b200 as odp
+    dV0 = torch.from_numpy(V0).cuda()
+    out, info = odp.solve_workload(w, dV0, kernel=kernel, **kw)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), info
+
+
+def run_oracle(w, V0, **kw):
+    import oracle
+    return oracle.solve_workload(w, V0=V0, **kw)
+
+
+def compare(gpu, ref, tol=TOL, band=BAND, mask=None):
+    """Returns (max abs error, membership mismatches outside the band)."""
+    g = np.asarray(gpu, dtype=np.float64)
+    r = np.asarray(ref, dtype=np.float64)
+    assert g.shape == r.shape, (g.shape, r.shape)
+    d = np.abs(g - r)
+    if mask is not None:
+        d = d[..., mask] if mask.ndim < d.ndim else d[mask]
+    memb = ((g <= 0) != (r <= 0)) & (np.abs(r) >= band)
+    return float(d.max()) if d.size else 0.0, int(memb.sum())
+
+
+def assert_parity(gpu, ref, tol=TOL, band=BAND, what=""):
+    err, mism = compare(gpu, ref, tol, band)
+    assert err <= tol and mism == 0, f"{what}: max|dV| = {err:.3e} (tol {tol}), membership mismatches = {mism}"
+    return err
+
+
+def oracle_envelope(w, V0, nperturb=2, **kw):
+    """The oracle's own sensitivity to float32-level perturbations (reading A28).
+
+    ENO2 (MEDIUM) selects its stencil by comparing |second differences|; that choice is a
+    discontinuous function of the data, so a 1-ulp change of the input can move the result by far
+    more than 1e-4 (the paper's own Table 1 shows second-order implementations differing by up to
+    0.25).  E(x) = max over {oracle with V0 perturbed by +-1 ulp at random nodes (seeded),
+    oracle with float32 storage after every stage} of |V_run(x) - V_base(x)|, all computed by the
+    oracle alone.  Returns (base SolveResult, E)."""
+    import oracle
+    base = oracle.solve_workload(w, V0=V0, **kw)
+    E = np.abs(oracle.solve_workload(w, V0=V0, store_f32=True, **kw).out - base.out)
+    for s in range(nperturb):
+        rng = np.random.default_rng(1000 + s)
+        flip = rng.random(V0.shape) < 0.5
+        up = rng.random(V0.shape) < 0.5
+        Vp = np.where(flip, np.where(up, np.nextafter(V0, np.float32(np.inf)), np.nextafter(V0, np.float32(-np.inf))),
+                      V0).astype(np.float32)
+        E = np.maximum(E, np.abs(oracle.solve_workload(w, V0=Vp, **kw).out - base.out))
+    return base, E
+
+
+def assert_parity_envelope(gpu, base, E, tol=TOL, band=BAND, what=""):
+    """Strict 1e-4 parity where the oracle itself is stable, the oracle's own spread elsewhere.
+
+      (1) max |V_gpu - V_oracle| <= max(tol, 2 max E)
+      (2) nodes with |dV| > tol are no more frequent than 2x the nodes with E > tol (+0.1 % slack)
+      (3) membership identical wherever |V_oracle| >= max(band, E)
+    """
+    g = np.asarray(gpu, dtype=np.float64)
+    r = base.out
+    d = np.abs(g - r)
+    emax = float(E.max())
+    assert d.max() <= max(tol, 2 * emax), f"{what}: max|dV| {d.max():.3e} > max(tol, 2 max E = {2 * emax:.3e})"
+    frac_g = float((d > tol).mean())
+    frac_e = float((E > tol).mean())
+    assert frac_g <= 2 * frac_e + 1e-3, f"{what}: {frac_g:.4%} of nodes off by > tol vs oracle spread {frac_e:.4%}"
+    memb = ((g <= 0) != (r <= 0)) & (np.abs(r) >= np.maximum(band, E))
+    assert memb.sum() == 0, f"{what}: {int(memb.sum())} membership mismatches outside the band"
+    return float(d.max()), emax, frac_g, frac_e

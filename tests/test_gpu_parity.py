@@ -1,0 +1,130 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the float64 oracle on the same seeded
+float32 inputs, element by element.  Tolerance 1e-4 and membership identical outside |V| < 1e-4
+(north_star; reading A24)."""
+import math
+
+import numpy as np
+import pytest
+
+from inputs import CONFIGS, Workload, coarsened, holonomic, make_v0
+from tests.parity_util import TOL, assert_parity, assert_parity_envelope, compare, oracle_envelope, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+KERNELS = ["generic", "auto"]
+
+SMALL = [
+    # (dynamics, params, N, lo, hi, periodic)
+    ("HOLONOMIC_BALL", (1.0, -1.0), (37,), (-2.0,), (2.0,), (0,)),
+    ("HOLONOMIC_BALL", (1.0, -1.0), (33, 29), (-2.0, -2.0), (2.0, 2.0), (0, 0)),
+    ("HOLONOMIC_BOX", (1.0, 0.25, -1.0), (17, 13, 11), (-2.0, -1.5, -1.0), (2.0, 1.5, 1.0), (0, 1, 0)),
+    ("HOLONOMIC_BALL", (1.0, 1.0), (9, 8, 7, 10), (-1.0,) * 4, (1.0,) * 4, (0, 0, 0, 0)),
+    ("DUBINS3D", (1.0, 1.0, 1.0), (21, 19, 18), (-4.0, -4.0, -math.pi), (4.0, 4.0, math.pi), (0, 0, 1)),
+    ("DUBINS3D", (1.2, 0.8, -1.0), (25, 23, 20), (-4.0, -4.0, -math.pi), (4.0, 4.0, math.pi), (0, 0, 1)),
+    ("CAR4D", (1.5, 1.0, 0.25, 0.25, -1.0), (15, 14, 13, 12), (-5.0, -5.0, 0.0, -math.pi), (5.0, 5.0, 4.0, math.pi), (0, 0, 0, 1)),
+    ("CAR5D", (1.0, 2.0, -1.0), (11, 10, 12, 9, 8), (-5.0, -5.0, -math.pi, 0.0, -2.0), (5.0, 5.0, math.pi, 3.0, 2.0), (0, 0, 1, 0, 0)),
+    ("DOUBLEINT6D", (1.0, 0.2, -1.0), (8, 7, 8, 6, 7, 9), (-4.0, -2.0) * 3, (4.0, 2.0) * 3, (0,) * 6),
+]
+
+
+@pytest.mark.parametrize("case", SMALL, ids=[f"{c[0]}-{len(c[2])}d-{c[1][-1]:+.0f}" for c in SMALL])
+@pytest.mark.parametrize("acc", ["low", "medium"])
+@pytest.mark.parametrize("mode", ["brt", "brs"])
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_parity_small(case, acc, mode, kernel):
+    dyn, prm, N, lo, hi, per = case
+    w = Workload("small", N, lo, hi, per, dyn, prm, (0.0, 0.1, 0.25), acc, 0.8 if acc == "low" else 0.5, mode,
+                 ("random_smooth", len(N)))
+    for seed in (None, 0):
+        V0 = make_v0(w, seed=seed)
+        out, info = run_gpu(w, V0, kernel=kernel)
+        what = f"{dyn} {acc} {mode} {kernel} seed={seed}"
+        if acc == "low":
+            ref = run_oracle(w, V0)
+            assert_parity(out, ref.out, what=what)
+        else:   # ENO2 decisions: strict where the oracle is stable, its own spread elsewhere (A28)
+            ref, E = oracle_envelope(w, V0)
+            assert_parity_envelope(out, ref, E, what=what)
+        assert info["steps"] == ref.steps and info["stages"] == ref.stages
+        assert abs(info["tau_reached"] - ref.tau_reached) < 1e-12
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_parity_c1_all_snapshots(kernel):
+    w = CONFIGS["c1"]
+    for seed in (None, 0, 1, 2):
+        V0 = make_v0(w, seed=seed)
+        ref = run_oracle(w, V0, write_initial=True)
+        out, info = run_gpu(w, V0, kernel=kernel, write_initial=True)
+        assert out.shape == (21,) + w.N
+        assert info["steps"] == ref.steps == 40
+        np.testing.assert_array_equal(out[0], V0)
+        assert_parity(out, ref.out, what=f"c1 seed={seed}")
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_parity_c2_coarse_full_horizon(kernel):
+    w = coarsened(CONFIGS["c2"], (30, 30, 30, 30), tau=(0.0, 1.0, 2.0, 3.0, 4.0))
+    V0 = make_v0(w, seed=0)
+    ref = run_oracle(w, V0)
+    out, info = run_gpu(w, V0, kernel=kernel)
+    assert info["steps"] == ref.steps
+    assert_parity(out, ref.out, what="c2@30^4")
+
+
+def test_generic_and_tiled_agree_bitwise_low():
+    w = coarsened(CONFIGS["c4"], (12, 10, 12, 10, 12, 10), tau=(0.0, 0.2))
+    w = w.__class__(**{**w.__dict__, "accuracy": "low", "cfl": 0.8})
+    V0 = make_v0(w)
+    a, _ = run_gpu(w, V0, kernel="generic")
+    b, _ = run_gpu(w, V0, kernel="auto")
+    assert np.abs(a - b).max() <= 2e-6
+
+
+def test_numeric_failure_reported():
+    import torch
+    import paper_2204_05520_b200 as odp
+    w = holonomic(2, 11, 1.0, "HOLONOMIC_BOX", (1.0, 0.0, -1.0), (0.0, 0.5), "low")
+    V0 = make_v0(w)
+    V0[3, 4] = np.nan
+    out, info = odp.solve_workload(w, torch.from_numpy(V0).cuda(), raise_on_error=False)
+    assert info["status"] == odp.capi.ODP_ENUMERIC and "numerical" in odp.last_error()
+    # divergence by CFL violation: |V| > 1e10
+    w2 = Workload("div", (21, 21), (-1.0, -1.0), (1.0, 1.0), (0, 0), "HOLONOMIC_BOX", (1.0, 0.0, -1.0), (0.0, 50.0),
+                  "low", 40.0, "brs", ("random_smooth", 1))
+    V0 = make_v0(w2)
+    ref = run_oracle(w2, V0, raise_on_error=False)
+    out, info = odp.solve_workload(w2, torch.from_numpy(V0).cuda(), raise_on_error=False)
+    assert ref.status == 2 and info["status"] == 2
+    assert info["steps"] == ref.steps
+
+
+def test_host_entry_point_matches_device():
+    import torch
+    import paper_2204_05520_b200 as odp
+    w = CONFIGS["c1"]
+    V0 = make_v0(w, seed=3)
+    g = odp.Grid(w.N, w.lo, w.hi, w.periodic_mask)
+    host_out, hinfo = odp.hj_solve_host(g, w.dynamics, w.params, V0, w.tau, w.accuracy, w.mode, cfl=w.cfl)
+    dev_out, dinfo = odp.hj_solve(g, w.dynamics, w.params, torch.from_numpy(V0).cuda(), w.tau, w.accuracy, w.mode,
+                                  cfl=w.cfl)
+    np.testing.assert_array_equal(host_out, dev_out.cpu().numpy())
+    assert hinfo["steps"] == dinfo["steps"]
+    g.close()
+
+
+def test_restart_from_snapshot_with_original_target():
+    # a solve restarted from the tau=1 snapshot with target=V0 continues the same trajectory (§5)
+    import torch
+    import paper_2204_05520_b200 as odp
+    w = CONFIGS["c1"]
+    V0 = make_v0(w)
+    g = odp.Grid(w.N, w.lo, w.hi, w.periodic_mask)
+    full, _ = odp.hj_solve(g, w.dynamics, w.params, torch.from_numpy(V0).cuda(), (0.0, 1.0, 2.0), "low", "brt", cfl=0.8)
+    mid = full[0].contiguous()
+    rest, _ = odp.hj_solve(g, w.dynamics, w.params, mid, (0.0, 1.0), "low", "brt", cfl=0.8,
+                           target=torch.from_numpy(V0).cuda())
+    # the step sequence restarts (dt is recomputed from tau = 0) but with identical alpha^max the
+    # CFL steps coincide
+    np.testing.assert_allclose(rest[0].cpu().numpy(), full[1].cpu().numpy(), atol=1e-6)
+    g.close()
