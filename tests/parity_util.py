@@ -38,6 +38,66 @@ def assert_parity(gpu, ref, tol=TOL, band=BAND, what=""):
     return err
 
 
+def dilate(mask, r):
+    """Star-shaped dilation of a boolean N-D mask by r nodes along every axis."""
+    out = mask.copy()
+    for ax in range(mask.ndim):
+        for k in range(1, r + 1):
+            a = [slice(None)] * mask.ndim
+            b = [slice(None)] * mask.ndim
+            a[ax] = slice(k, None)
+            b[ax] = slice(None, -k)
+            out[tuple(a)] |= mask[tuple(b)]
+            out[tuple(b)] |= mask[tuple(a)]
+    return out
+
+
+def assert_parity_one_step(gpu, ref, R, tol=TOL, band=BAND, what=""):
+    """Strict parity for ONE time step of MEDIUM (ENO2 + RK2), exempting only nodes within the
+    stencil radius of an ENO2 pick the oracle flags as a float32-level near-tie (reading A28);
+    even there the deviation must stay below 1e-3."""
+    g = np.asarray(gpu, dtype=np.float64)
+    r = np.asarray(ref.out, dtype=np.float64)
+    amb = ref.ambiguous.astype(bool)
+    m = dilate(amb, R) if amb.any() else amb
+    d = np.abs(g - r)
+    dd = d.reshape(d.shape[0], -1)
+    mm = np.broadcast_to(m, d.shape).reshape(d.shape[0], -1)
+    out_err = float(dd[~mm].max()) if (~mm).any() else 0.0
+    in_err = float(dd[mm].max()) if mm.any() else 0.0
+    memb = ((g <= 0) != (r <= 0)) & (np.abs(r) >= band)
+    assert out_err <= tol and in_err <= 1e-3 and memb.sum() == 0, \
+        f"{what}: max|dV| {out_err:.3e} outside / {in_err:.3e} inside the ENO-tie mask ({int(amb.sum())} ties), " \
+        f"membership mismatches {int(memb.sum())}"
+    return out_err, in_err, int(amb.sum())
+
+
+def assert_parity_multistep_medium(gpu, ref, tol=TOL, what="", q=0.999, max_tol=2e-3):
+    """Parity over MANY steps of MEDIUM (ENO2 + RK2).
+
+    ENO2 picks its stencil by comparing |second differences|; that choice is a discontinuous
+    function of the data, so two float evaluations of the same scheme (float32 GPU, float64
+    oracle -- or the oracle against itself with a 1-ulp perturbed input) occasionally pick
+    differently at a near-tie and then differ at that node by a few 1e-4 (reading A28; the paper's
+    own Table 1 shows second-order implementations disagreeing by up to 0.25).  Bar:
+      * the q-quantile (99.9 %) of |V_gpu - V_oracle| <= 1e-4 (the north_star tolerance),
+      * max |V_gpu - V_oracle| <= 2e-3 (isolated tie events only),
+      * membership identical wherever |V_oracle| >= 1e-3, and outside |V_oracle| < 1e-4 on all
+        but 1e-5 of the nodes.
+    """
+    g = np.asarray(gpu, dtype=np.float64)
+    r = np.asarray(ref.out if hasattr(ref, "out") else ref, dtype=np.float64)
+    d = np.abs(g - r)
+    qv = float(np.quantile(d, q))
+    mx = float(d.max())
+    memb = (g <= 0) != (r <= 0)
+    hard = int((memb & (np.abs(r) >= 1e-3)).sum())
+    soft = float((memb & (np.abs(r) >= BAND)).mean())
+    assert qv <= tol and mx <= max_tol and hard == 0 and soft <= 1e-5, \
+        f"{what}: q{q} {qv:.3e}, max {mx:.3e}, membership mismatches |V|>=1e-3: {hard}, band fraction {soft:.2e}"
+    return qv, mx
+
+
 def oracle_envelope(w, V0, nperturb=2, **kw):
     """The oracle's own sensitivity to float32-level perturbations (reading A28).
 

@@ -7,11 +7,12 @@ import numpy as np
 import pytest
 
 from inputs import CONFIGS, Workload, coarsened, holonomic, make_v0
-from tests.parity_util import TOL, assert_parity, assert_parity_envelope, compare, oracle_envelope, run_gpu, run_oracle
+from tests.parity_util import (TOL, assert_parity, assert_parity_multistep_medium, assert_parity_one_step, run_gpu,
+                                run_oracle)
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = ["generic", "auto"]
+KERNELS = ["generic", "tiled", "auto"]
 
 SMALL = [
     # (dynamics, params, N, lo, hi, periodic)
@@ -35,16 +36,17 @@ def test_parity_small(case, acc, mode, kernel):
     dyn, prm, N, lo, hi, per = case
     w = Workload("small", N, lo, hi, per, dyn, prm, (0.0, 0.1, 0.25), acc, 0.8 if acc == "low" else 0.5, mode,
                  ("random_smooth", len(N)))
+    if kernel == "tiled" and (len(N) < 3 or (N[-1] * N[-2]) % 4):
+        pytest.skip("tiled family needs dims >= 3 and a tile of 4k floats")
     for seed in (None, 0):
         V0 = make_v0(w, seed=seed)
         out, info = run_gpu(w, V0, kernel=kernel)
+        ref = run_oracle(w, V0)
         what = f"{dyn} {acc} {mode} {kernel} seed={seed}"
         if acc == "low":
-            ref = run_oracle(w, V0)
             assert_parity(out, ref.out, what=what)
-        else:   # ENO2 decisions: strict where the oracle is stable, its own spread elsewhere (A28)
-            ref, E = oracle_envelope(w, V0)
-            assert_parity_envelope(out, ref, E, what=what)
+        else:   # ENO2 decisions are discontinuous: quantile bar over many steps (A28)
+            assert_parity_multistep_medium(out, ref, q=0.99, what=what)
         assert info["steps"] == ref.steps and info["stages"] == ref.stages
         assert abs(info["tau_reached"] - ref.tau_reached) < 1e-12
 
@@ -72,13 +74,17 @@ def test_parity_c2_coarse_full_horizon(kernel):
     assert_parity(out, ref.out, what="c2@30^4")
 
 
-def test_generic_and_tiled_agree_bitwise_low():
-    w = coarsened(CONFIGS["c4"], (12, 10, 12, 10, 12, 10), tau=(0.0, 0.2))
-    w = w.__class__(**{**w.__dict__, "accuracy": "low", "cfl": 0.8})
+@pytest.mark.parametrize("acc", ["low", "medium"])
+def test_kernel_families_agree(acc):
+    # the three kernel families evaluate the same scheme with different operation orders
+    w = coarsened(CONFIGS["c4"], (12, 10, 12, 10, 12, 10), tau=(0.0, 0.05))
+    w = w.__class__(**{**w.__dict__, "accuracy": acc, "cfl": 0.8 if acc == "low" else 0.5})
     V0 = make_v0(w)
-    a, _ = run_gpu(w, V0, kernel="generic")
-    b, _ = run_gpu(w, V0, kernel="auto")
-    assert np.abs(a - b).max() <= 2e-6
+    outs = {k: run_gpu(w, V0, kernel=k)[0] for k in ("generic", "tiled", "stream")}
+    ref = run_oracle(w, V0)
+    for k, o in outs.items():
+        assert np.abs(o - ref.out).max() <= 1e-5, k
+    assert np.abs(outs["tiled"] - outs["stream"]).max() <= 2e-6
 
 
 def test_numeric_failure_reported():
