@@ -1,0 +1,993 @@
+// kernels_march.cuh -- the "march" kernel family (default) of the B200 HJ level-set step.
+//
+// Decomposition: a CTA owns a COLUMN of in-plane tiles (the two innermost, contiguous axes) at
+// fixed indices of the "side" outer axes and marches the innermost outer axis (the MARCHING axis).
+// Every tile a step reads -- the centre tile (row block + halo rows) and the 2R side-neighbour
+// tiles per side axis -- is staged in shared memory by 1-D TMA bulk copies (cp.async.bulk, one
+// lane of warp 0 per copy, completion on an mbarrier), issued one step ahead into double buffers,
+// so threads read every stencil neighbour with a plain LDS at a fixed per-thread offset (the
+// stream family spent ~45 % of its instructions on 64-bit global address arithmetic).  What the
+// arithmetic does differently from the stream / generic families:
+//
+//  * EDGE SHARING.  The ENO2 selection of an edge i+1/2, m = pick(d2_i, d2_{i+1}), and its first
+//    difference d1 = v_{i+1} - v_i give BOTH D+_i = d1 - m/2 and D-_{i+1} = d1 + m/2 (in units
+//    of h; §3.4.4, reading A13).  Along the marching axis the edge of the previous step is
+//    carried in registers (one second difference, one pick per node instead of three and two);
+//    along the in-plane column axis the VEC nodes of a thread share their interior edges.
+//  * EDGE-ASSIGNED PASS 1.  Pass 1 only needs the global range of {D-_i, D+_i} (Alg. 2
+//    l.157-158, A4).  Every value is one side of an edge, so a node contributes its upper edge
+//    (both sides) -- 3 loads, 2 second differences, 1 pick per side axis instead of 4, 3, 2 --
+//    and min(D+, D-) = d1 - |m|/2, max = d1 + |m|/2 (exact: one of the two fma's).  Nodes on a
+//    face add the one-sided values of the face edges (min/max are idempotent, so a value seen
+//    twice is harmless; the only thing to avoid is a value that is not a node's D-/D+).
+//  * PACKED FP32.  Two adjacent nodes of a row are one float2; every add/mul/fma on node pairs is
+//    one FADD2/FMUL2/FFMA2 (sm_100a), the ENO picks are FSETP+FSEL per node, the range
+//    accumulation is 3-input FMNMX3.
+//  * NO CTA BARRIER IN THE LOOP.  One producer warp issues the copies and waits on "empty"
+//    mbarriers (one arrive per compute warp and step); compute warps wait only on the "full"
+//    mbarrier of their step, so warps drift freely within the two-stage pipeline.  In-plane ghost
+//    cells (A12) are formed in registers by the threads on the tile faces (periodic halo rows are
+//    copied by TMA, periodic columns read wrapped offsets).
+//
+// The arithmetic of every D-/D+ is the same sequence of IEEE float32 operations as in the stream
+// and generic families (d2 = fma(-2, v_c, v_l + v_r); D = fma(+-0.5, m, d1)), so the derivative
+// range of pass 1 is bit-identical across families.
+//
+//   pass 1 (PASS2=false): min/max of hD-/hD+ per axis, max|W| (NaN-propagating), per-CTA partials
+//   pass 2 (PASS2=true):  p, H, alpha_i, dissipation, Euler/RK stage, BRT min (Alg. 2 l.153-169)
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
+
+#include "kernels_stream.cuh"
+
+namespace odp {
+
+#ifndef ODP_MARCH_MINB1
+#define ODP_MARCH_MINB1 2      // CTAs/SM the register budget of the NP=1 (VEC=2) kernels is sized for
+#endif
+#ifndef ODP_MARCH_MINB2
+#define ODP_MARCH_MINB2 1      // ... and of the NP=2 (VEC=4) kernels
+#endif
+#ifndef ODP_MARCH_SELP
+#define ODP_MARCH_SELP 0       // 1: ENO pick as FSET + 3 FMA-pipe ops instead of FSETP + FSEL
+#endif
+constexpr int MARCH_MAXT1 = 512;   // threads per CTA, NP = 1
+constexpr int MARCH_MAXT2 = 640;   // threads per CTA, NP = 2
+
+// ---- packed fp32 helpers (FADD2 / FMUL2 / FFMA2 on sm_100a) -------------------------------------
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 f2s(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+// second difference d2 = fma(-2, c, l + r)  (bitwise the same as the scalar families)
+__device__ __forceinline__ float2 d2p(float2 l, float2 c, float2 r) { return fma2(f2s(-2.f), c, add2(l, r)); }
+__device__ __forceinline__ float d2s(float l, float c, float r) { return fmaf(-2.f, c, l + r); }
+
+// A13: the smaller second difference in magnitude, the left one on ties
+__device__ __forceinline__ float pick1(float a, float b) {
+#if ODP_MARCH_SELP
+    float p;   // p = 1 if |a| <= |b| else 0; a p + b (1 - p) is exact (one of the products is 0)
+    asm("set.le.f32.f32 %0, %1, %2;" : "=f"(p) : "f"(fabsf(a)), "f"(fabsf(b)));
+    return fmaf(b, 1.f - p, a * p);
+#else
+    return fabsf(a) <= fabsf(b) ? a : b;
+#endif
+}
+__device__ __forceinline__ float2 pick2(float2 a, float2 b) { return f2(pick1(a.x, b.x), pick1(a.y, b.y)); }
+
+// |x| on the FMA pipe (FADD RZ, |x|) rather than a LOP on the ALU pipe
+__device__ __forceinline__ float absf(float x) { return fabsf(x) + 0.f; }
+__device__ __forceinline__ float2 abs2(float2 a) { return f2(absf(a.x), absf(a.y)); }
+
+__device__ __forceinline__ float min3f(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ float max3nan(float a, float b, float c) {   // NaN-propagating (guard A19)
+    float r;
+    asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+// range of the two sides of an edge {d1 - m/2, d1 + m/2} into [mn, mx] (both nodes of a pair)
+__device__ __forceinline__ void inc_edge(float2 m, float2 d1, float &mn, float &mx) {
+    const float2 am = abs2(m);
+    const float2 lo = fma2(f2s(-0.5f), am, d1), hi = fma2(f2s(0.5f), am, d1);
+    mn = min3f(mn, lo.x, lo.y);
+    mx = max3f(mx, hi.x, hi.y);
+}
+__device__ __forceinline__ void inc_val(float2 v, float &mn, float &mx) {
+    mn = min3f(mn, v.x, v.y);
+    mx = max3f(mx, v.x, v.y);
+}
+__device__ __forceinline__ void inc_s(float v, float &mn, float &mx) {
+    mn = fminf(mn, v);
+    mx = fmaxf(mx, v);
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// 1-D TMA bulk copy global -> shared (CTA-local destination address), completing on an mbarrier
+__device__ __forceinline__ void tma_bulk_g2s_u32(uint32_t dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// ghost value (A12) for a pair
+__device__ __forceinline__ float2 ghost2(float2 e, float2 in, float q) { return f2(ghost(e.x, in.x, q), ghost(e.y, in.y, q)); }
+
+// Fix the out-of-domain slots of a pair window x[0..2R] centred on index i of an axis of extent N
+// (non-periodic): the pair version of fix_ghosts.
+template <int R>
+__device__ __forceinline__ void fix_ghosts2(float2 *x, int i, int N) {
+    float xs[2 * R + 1], ys[2 * R + 1];
+#pragma unroll
+    for (int k = 0; k <= 2 * R; ++k) { xs[k] = x[k].x; ys[k] = x[k].y; }
+    fix_ghosts<R>(xs, i, N);
+    fix_ghosts<R>(ys, i, N);
+#pragma unroll
+    for (int k = 0; k <= 2 * R; ++k) x[k] = f2(xs[k], ys[k]);
+}
+
+// ---- vector memory helpers: NP float2 pairs = 2 NP consecutive floats ---------------------------
+template <int NP>
+__device__ __forceinline__ void ldg_p(const float *p, float2 *v) {
+    if constexpr (NP == 2) {
+        const float4 t = __ldg(reinterpret_cast<const float4 *>(p));
+        v[0] = f2(t.x, t.y); v[1] = f2(t.z, t.w);
+    } else {
+        v[0] = __ldg(reinterpret_cast<const float2 *>(p));
+    }
+}
+template <int NP>
+__device__ __forceinline__ void ldg_plain(const float *p, float2 *v) {   // coherent load (may alias out)
+    if constexpr (NP == 2) {
+        const float4 t = *reinterpret_cast<const float4 *>(p);
+        v[0] = f2(t.x, t.y); v[1] = f2(t.z, t.w);
+    } else {
+        v[0] = *reinterpret_cast<const float2 *>(p);
+    }
+}
+template <int NP>
+__device__ __forceinline__ void lds_p(const float *p, float2 *v) {
+    if constexpr (NP == 2) {
+        const float4 t = *reinterpret_cast<const float4 *>(p);
+        v[0] = f2(t.x, t.y); v[1] = f2(t.z, t.w);
+    } else {
+        v[0] = *reinterpret_cast<const float2 *>(p);
+    }
+}
+template <int NP>
+__device__ __forceinline__ void st_p(float *p, const float2 *v) {
+    if constexpr (NP == 2) *reinterpret_cast<float4 *>(p) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+    else *reinterpret_cast<float2 *>(p) = v[0];
+}
+
+// ---- pass-2 per-axis terms ----------------------------------------------------------------------
+// Every compiled-in functor except the ball has a separable Hamiltonian
+//     H = sum_d [ c_d(x) p_d + k_d |p_d| ]     (table C-2; Eq. 4 with bang-bang u*, d*)
+// with p_d = (D-_d + D+_d)/2 (A3); c_d, k_d below.  The ball accumulates sum p_d^2 (H = kH |p|_2).
+// Inputs are s = h(D- + D+) and t = h(D+ - D-); hih = 1/(2h).
+template <class F> struct Sep { static constexpr bool ball = false; };
+template <int N> struct Sep<FHoloBall<N>> { static constexpr bool ball = true; };
+
+template <int NDIM> __device__ __forceinline__ float lin_c(const FHoloBox<NDIM> &, int, const Pt &) { return 0.f; }
+template <int NDIM> __device__ __forceinline__ float abs_k(const FHoloBox<NDIM> &f, int) { return f.kH; }
+template <int NDIM> __device__ __forceinline__ float lin_c(const FHoloBall<NDIM> &, int, const Pt &) { return 0.f; }
+template <int NDIM> __device__ __forceinline__ float abs_k(const FHoloBall<NDIM> &, int) { return 0.f; }
+__device__ __forceinline__ float lin_c(const FDubins3D &f, int d, const Pt &q) {
+    return d == 0 ? f.v * q.c[2] : (d == 1 ? f.v * q.s[2] : 0.f);
+}
+__device__ __forceinline__ float abs_k(const FDubins3D &f, int d) { return d == 2 ? f.kw : 0.f; }
+__device__ __forceinline__ float lin_c(const FCar4D &, int d, const Pt &q) {
+    return d == 0 ? q.x[2] * q.c[3] : (d == 1 ? q.x[2] * q.s[3] : 0.f);
+}
+__device__ __forceinline__ float abs_k(const FCar4D &f, int d) {
+    return d == 0 ? f.kdx : (d == 1 ? f.kdy : (d == 2 ? f.ka : f.kw));
+}
+__device__ __forceinline__ float lin_c(const FCar5D &, int d, const Pt &q) {
+    return d == 0 ? q.x[3] * q.c[2] : (d == 1 ? q.x[3] * q.s[2] : (d == 2 ? q.x[4] : 0.f));
+}
+__device__ __forceinline__ float abs_k(const FCar5D &f, int d) { return d == 3 ? f.ka : (d == 4 ? f.kal : 0.f); }
+__device__ __forceinline__ float lin_c(const FDoubleInt6D &, int d, const Pt &q) { return (d & 1) == 0 ? q.x[d + 1] : 0.f; }
+__device__ __forceinline__ float abs_k(const FDoubleInt6D &f, int d) { return (d & 1) ? f.kv : 0.f; }
+
+// compile-time masks of the axes with a linear / an absolute-value term
+template <class F> struct Terms { static constexpr unsigned LIN = 0, ABS = 0x3f; };   // holonomic box
+template <int N> struct Terms<FHoloBall<N>> { static constexpr unsigned LIN = 0, ABS = 0; };
+template <> struct Terms<FDubins3D> { static constexpr unsigned LIN = 0x3, ABS = 0x4; };
+template <> struct Terms<FCar4D> { static constexpr unsigned LIN = 0x3, ABS = 0xf; };
+template <> struct Terms<FCar5D> { static constexpr unsigned LIN = 0x7, ABS = 0x18; };
+template <> struct Terms<FDoubleInt6D> { static constexpr unsigned LIN = 0x15, ABS = 0x2a; };
+
+template <class F>
+__device__ __forceinline__ void axis_terms(const F &f, int d, const Pt &q0, const Pt &q1, float hih, float2 u,
+                                           float2 w, float2 &acc, float2 &dis) {
+    const float2 s = add2(u, w), t = sub2(w, u);
+    if constexpr (Sep<F>::ball) {
+        const float2 sh = mul2(s, f2s(hih));
+        acc = fma2(sh, sh, acc);
+    } else {
+        if ((Terms<F>::LIN >> d) & 1) acc = fma2(s, f2(lin_c(f, d, q0) * hih, lin_c(f, d, q1) * hih), acc);
+        if ((Terms<F>::ABS >> d) & 1) {
+            const float k = abs_k(f, d) * hih;
+            acc = f2(fmaf(fabsf(s.x), k, acc.x), fmaf(fabsf(s.y), k, acc.y));
+        }
+    }
+    dis = fma2(t, f2(f.alpha(d, q0) * hih, f.alpha(d, q1) * hih), dis);
+}
+
+template <class F>
+__device__ __forceinline__ float2 ham_fin2(const F &f, float2 acc) {
+    if constexpr (Sep<F>::ball) return f2(f.kH * sqrtf(acc.x), f.kH * sqrtf(acc.y));
+    else return acc;
+}
+
+// ---- kernel -------------------------------------------------------------------------------------
+//
+// Unit of work: (column, marching segment, row block).  A COLUMN fixes the side-axis indices; the
+// CTA marches the marching axis over the segment; a ROW BLOCK is B consecutive rows of the in-plane
+// tile (B = N2 when the whole tile fits the CTA).  Shared memory per CTA:
+//   ring  RS = R+2 slots, each the row block +-R halo rows of one centre tile (the tile of marching
+//         index j is the centre of step j; slot = step counter mod RS);
+//   side  2 buffers x NSS slots (NSS = 2R per side axis), each the row block of one side-neighbour
+//         tile of the current step;
+//   bars  two mbarriers (one per buffer parity).
+// Warp 0 issues every copy as a 1-D TMA bulk copy (cp.async.bulk, one lane per copy) one step
+// ahead: while step j computes, the tiles of step j+1 are in flight.  A thread's stencil
+// neighbours are then plain LDS at fixed per-thread offsets -- no global address arithmetic in the
+// loop (the stream family spent ~45 % of its instructions there).
+struct MarchArgs {
+    int M, N2, N1;        // tile size and in-plane extents
+    int per2, per1;
+    int QR;               // threads per row = N1 / VEC
+    int B, nrb;           // rows per row block, row blocks per tile
+    int nthr;             // B * QR
+    int RSZ, SSZ;         // floats per ring / side slot
+    int NSS;              // side slots per buffer (2R per side axis)
+    int rmarg;            // leading margin of a ring slot (keeps TMA destinations 16-B aligned)
+    int side_off;         // float offset of the side buffers
+    int bar_off;          // float offset of the mbarriers
+    int tab_off;          // float offset of the per-unit copy table
+    int K, nseg, units;   // marching segment length, segments per column, work units
+};
+constexpr int MARCH_SMARG = 4;   // leading margin of a side slot (floats)
+
+// Shared-memory geometry of a CTA (floats), a function of (R, N1, B, NSS) only; used by the host
+// plan and -- for the shape-specialised instances -- as compile-time constants in the kernel, so
+// every stencil read is an LDS at an immediate offset from one per-thread base register.
+__host__ __device__ constexpr int geo_rmarg(int R, int N1) { return 4 + ((-R * N1) & 3); }
+__host__ __device__ constexpr int geo_rsz(int R, int N1, int B) {
+    return ((geo_rmarg(R, N1) + (B + 2 * R) * N1 + 4 + 3) / 4) * 4;
+}
+__host__ __device__ constexpr int geo_ssz(int N1, int B) { return ((MARCH_SMARG + B * N1 + 3) / 4) * 4; }
+__host__ __device__ constexpr int geo_side_off(int R, int N1, int B) { return (R + 2) * geo_rsz(R, N1, B); }
+__host__ __device__ constexpr int geo_bar_off(int R, int N1, int B, int NSS) {
+    return ((geo_side_off(R, N1, B) + 2 * NSS * geo_ssz(N1, B)) + 3) / 4 * 4;
+}
+// 4 mbarriers (32 B) + copy table: 32 x 8 B offsets + 32 x 4 B sizes + 8 x 4 B ring fields
+__host__ __device__ constexpr int geo_smem_bytes(int R, int N1, int B, int NSS) {
+    return geo_bar_off(R, N1, B, NSS) * 4 + 32 + 32 * 8 + 32 * 4 + 8 * 4;
+}
+
+struct MarchUnit {
+    int col, seg, rb, r0, nrow;   // column, segment, row block, first row, rows owned
+    int m0, m1;                   // global marching range of the segment
+    long long cbase;              // element offset of the column's tile at local marching index 0
+};
+
+__device__ __forceinline__ MarchUnit march_unit(const MarchArgs &a, int Nml, int mlo, int u) {
+    MarchUnit U;
+    const int rb = u % a.nrb;
+    const int cs = u / a.nrb;
+    U.col = cs / a.nseg;
+    U.seg = cs - U.col * a.nseg;
+    U.rb = rb;
+    U.r0 = rb * a.B;
+    U.nrow = min(a.B, a.N2 - U.r0);
+    U.m0 = mlo + U.seg * a.K;
+    U.m1 = min(mlo + Nml, U.m0 + a.K);
+    U.cbase = (long long)U.col * Nml * a.M;
+    return U;
+}
+
+template <class F, int NDIM, int R, int NP, bool PASS2, int CN1 = 0, int CB = 0>
+__global__ void __launch_bounds__(NP == 1 ? MARCH_MAXT1 : MARCH_MAXT2, NP == 1 ? ODP_MARCH_MINB1 : ODP_MARCH_MINB2)
+k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, const float *__restrict__ T,
+        float *out, float *partials, const DevState *st, FParams fp, int kind, int brt) {
+    if (!st->active) return;
+    constexpr int VEC = 2 * NP;
+    constexpr int NO = NDIM - 2;     // outer axes
+    constexpr int MA = NO - 1;       // marching axis; axes 0..MA-1 are the side axes
+    constexpr int NSA = MA > 0 ? MA : 1;
+    constexpr int RS = R + 2;        // ring slots
+    constexpr bool CT = CN1 > 0;     // shape-specialised instance: geometry known at compile time
+    constexpr int NSS_CT = 2 * R * MA;
+    extern __shared__ __align__(128) float smem[];
+    const int N1 = CT ? CN1 : a.N1;
+    const int RSZ = CT ? geo_rsz(R, CN1, CB) : a.RSZ;
+    const int SSZ = CT ? geo_ssz(CN1, CB) : a.SSZ;
+    const int RMG = CT ? geo_rmarg(R, CN1) : a.rmarg;
+    const int NSS = NSS_CT;
+    float *ring = smem;
+    float *side = smem + (CT ? geo_side_off(R, CN1, CB) : a.side_off);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + a.bar_off);
+
+    float mn[NDIM], mx[NDIM], mabs = 0.f;
+#pragma unroll
+    for (int d = 0; d < NDIM; ++d) { mn[d] = __int_as_float(0x7f800000); mx[d] = -__int_as_float(0x7f800000); }
+    F f;
+    float dt = 0.f;
+    const float *hih = g.hih;                 // 1/(2h) per axis (kernel-parameter space)
+    if constexpr (PASS2) {
+        f.init(fp, st->minD, st->maxD);
+        dt = st->dt_f;
+    }
+
+    const int N2 = a.N2, M = a.M;
+    const int QR = N1 / VEC;
+    const int tid = threadIdx.x;
+    const int lrow = tid / QR;                         // row within the row block
+    const int qc0 = (tid - lrow * QR) * VEC;           // first column of this thread's nodes
+    const int loff = (a.per1 && qc0 == 0) ? N1 - 2 : -2;              // left pair (cols c0-2, c0-1)
+    const int roff = (a.per1 && qc0 + VEC == N1) ? VEC - N1 : VEC;    // right pair (cols c0+VEC, +1)
+    const bool clo = !a.per1 && qc0 == 0, chi = !a.per1 && qc0 + VEC == N1;
+    const int toff = RMG + (lrow + R) * N1 + qc0;      // this thread's nodes in a ring slot
+    const int sloc = MARCH_SMARG + lrow * N1 + qc0;    // ... in a side slot
+    Pt qcv[VEC];                                       // in-plane column coordinates (pass 2)
+    if constexpr (PASS2) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) load_axis<F>(g, qcv[j], NDIM - 1, qc0 + j);
+    }
+
+    const int Nm = MA == 0 ? g.Ng0 : g.N[MA];       // marching extent (global: face tests)
+    const int mlo = MA == 0 ? g.g0 : 0;              // global index of local marching index 0
+    const int Nml = MA == 0 ? g.N[0] : g.N[MA];      // locally owned marching extent
+    const bool mper = g.per[MA] != 0;
+    auto mloc = [&](int jg) -> int {                 // local marching index of global jg (clamped / wrapped)
+        int j = jg;
+        if (j < 0 || j >= Nm) {
+            if (mper) j = j < 0 ? j + Nm : j - Nm;
+            else j = j < 0 ? 0 : Nm - 1;
+        }
+        return j - mlo;
+    };
+    // side-axis geometry of a column: global index and extent per side axis
+    auto side_geom = [&](int col, int *oid, int *oN) {
+        int r = col;
+#pragma unroll
+        for (int o = MA - 1; o >= 1; --o) { const int qv = r / g.N[o]; oid[o] = r - qv * g.N[o]; oN[o] = g.N[o]; r = qv; }
+        if constexpr (MA >= 1) { oid[0] = g.g0 + r; oN[0] = g.Ng0; }
+    };
+
+    // ---- copy issue (warp 0) ----
+    // Per unit, warp 0 fills a table of the unit's copies (lane l < NSS: side slot l; lane NSS:
+    // the ring tile).  Step j of the unit then needs: side slot l <- tile(j) + soff[l]; ring slot
+    // <- tile(j + R) (or, at the unit's first step, tiles j .. j + R).
+    long long *t_soff = reinterpret_cast<long long *>(smem + a.tab_off);   // [32]
+    uint32_t *t_snb = reinterpret_cast<uint32_t *>(t_soff + 32);           // [32] bytes (0 = skip)
+    int *t_ring = reinterpret_cast<int *>(t_snb + 32);                      // [8]: fa, nbytes, dst0, wrap-lo bytes, wrap-hi bytes, wrap-hi dst
+    auto make_table = [&](const MarchUnit &U) {
+        const int lane = tid & 31;
+        int oid[NSA], oN[NSA];
+        side_geom(U.col, oid, oN);
+        if (lane < NSS) {
+            const int o = lane / (2 * R), kk = lane - o * 2 * R;
+            const int k = kk < R ? kk - R : kk - R + 1;
+            int io = 0, no = 1, per = 0;
+            long long so = 0;
+#pragma unroll
+            for (int q = 0; q < MA; ++q)
+                if (q == o) { io = oid[q]; no = oN[q]; per = g.per[q]; so = g.stride[q]; }
+            const bool face = !per && (io < R || io > no - 1 - R);
+            int jo = io + k;
+            bool ok = true;
+            if (jo < 0 || jo >= no) {
+                if (per) jo = jo < 0 ? jo + no : jo - no;
+                else ok = false;
+            }
+            if (!PASS2 && R == 2 && !face && k == -2) ok = false;     // pass 1 interior: edge i+1/2 only
+            t_soff[lane] = (long long)(jo - io) * so + (long long)U.r0 * N1;
+            t_snb[lane] = ok ? (uint32_t)U.nrow * N1 * 4 : 0u;
+        }
+        if (lane == 0) {
+            const int va = U.r0 - R, vb = U.r0 + U.nrow + R;          // virtual rows [va, vb) of a ring slot
+            const int ra = max(va, 0), rbb = min(vb, N2);
+            int fa = ra * N1, fb = rbb * N1;
+            fa &= ~3; fb = (fb + 3) & ~3;                              // 16-B granules inside the tile
+            t_ring[0] = fa;
+            t_ring[1] = (fb - fa) * 4;
+            t_ring[2] = RMG + fa - va * N1;                        // destination float offset in the slot
+            t_ring[3] = (a.per2 && va < 0) ? (-va) * N1 * 4 : 0;
+            t_ring[4] = (a.per2 && vb > N2) ? (vb - N2) * N1 * 4 : 0;
+            t_ring[5] = RMG + (N2 - va) * N1;
+            t_ring[6] = (N2 + va) * N1;                                // wrap-lo source row offset
+        }
+        __syncwarp();
+    };
+    // copies of step `itx` = marching index j of unit U (ring tiles j+kb .. j+R)
+    auto issue = [&](const MarchUnit &U, int j, int itx, int kb) {
+        const int lane = tid & 31;
+        uint64_t *bar = &bars[itx & 1];
+        const long long tj = U.cbase + (long long)(j - mlo) * M;
+        uint32_t nb = 0, nbw0 = 0, nbw1 = 0;
+        const float *src = nullptr;
+        uint32_t dst = 0;
+        long long tt = 0;
+        float *slot = nullptr;
+        if (lane < NSS) {
+            nb = t_snb[lane];
+            src = W + tj + t_soff[lane];
+            dst = smem_u32(side + (itx & 1) * NSS * SSZ + lane * SSZ + MARCH_SMARG);
+        } else if (lane - NSS >= kb && lane - NSS <= R) {
+            const int k = lane - NSS, mj = j + k;
+            if (mj < U.m1) {
+                tt = U.cbase + (long long)mloc(mj) * M;
+                slot = ring + ((itx + k) % RS) * RSZ;
+                nb = (uint32_t)t_ring[1];
+                src = W + tt + t_ring[0];
+                dst = smem_u32(slot + t_ring[2]);
+                nbw0 = (uint32_t)t_ring[3];
+                nbw1 = (uint32_t)t_ring[4];
+            }
+        }
+        const uint32_t total = __reduce_add_sync(0xffffffffu, nb + nbw0 + nbw1);
+        if (lane == 0) mbar_expect_tx(bar, total);
+        __syncwarp();
+        if (nb) tma_bulk_g2s_u32(dst, src, nb, bar);
+        if (nbw0) tma_bulk_g2s_u32(smem_u32(slot + RMG), W + tt + t_ring[6], nbw0, bar);
+        if (nbw1) tma_bulk_g2s_u32(smem_u32(slot + t_ring[5]), W + tt, nbw1, bar);
+    };
+
+    // ---- warp roles: warps [0, nwc) compute, warp nwc issues the copies (producer) ----
+    // full[b]: the copies of a step with parity b landed (producer arrive + tx bytes);
+    // empty[b]: every compute warp finished reading that step's buffers (one arrive per warp).
+    const int nwc = (a.nthr + 31) >> 5;
+    uint64_t *full = bars, *empty = bars + 2;
+    if (tid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_init(&empty[0], nwc);
+        mbar_init(&empty[1], nwc);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if ((tid >> 5) == nwc) {                        // producer warp
+        int sp = 0;
+        for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+            const MarchUnit U = march_unit(a, Nml, mlo, u);
+            make_table(U);
+            for (int jg = U.m0; jg < U.m1; ++jg, ++sp) {
+                if (sp >= 2) mbar_wait(&empty[sp & 1], (uint32_t)(((sp >> 1) & 1) ^ 1));
+                issue(U, jg, sp, jg == U.m0 ? 0 : R);
+            }
+        }
+    }
+
+    int it = 0;                                      // step counter of this CTA (buffer / phase)
+    int rs0 = 0;                                     // it % RS: ring slot of the current centre tile
+    const float *rbase = ring + toff;
+    const float *sbase = side + sloc;
+    for (int u = blockIdx.x; u < a.units && (tid >> 5) < nwc; u += gridDim.x) {
+        const MarchUnit U = march_unit(a, Nml, mlo, u);
+        const int m0 = U.m0, m1 = U.m1;
+        const bool act = lrow < U.nrow && tid < a.nthr;
+        const int grow = U.r0 + lrow;                 // global row of this thread
+        const bool rlo = !a.per2 && grow < R, rhi = !a.per2 && grow > N2 - 1 - R;
+        int oid[NSA], oN[NSA];
+        side_geom(U.col, oid, oN);
+        bool oface[NSA];
+#pragma unroll
+        for (int o = 0; o < MA; ++o) oface[o] = !g.per[o] && (oid[o] < R || oid[o] > oN[o] - 1 - R);
+        Pt qrow;
+        if constexpr (PASS2) {
+#pragma unroll
+            for (int o = 0; o < MA; ++o) load_axis<F>(g, qrow, o, oid[o]);
+            load_axis<F>(g, qrow, NDIM - 2, min(grow, N2 - 1));
+        }
+        const float *cb = W + U.cbase + grow * N1 + qc0;   // this thread's nodes at local marching index 0
+
+        // ---- preamble: the window around m0 and the carried edge m0 - 1/2 (registers) ----
+        float2 win[R + 1][NP];
+        float2 dd0[NP], mL[NP], dL[NP], gE[NP], gS[NP];
+        if (act) {
+            float2 x[2 * R + 1][NP];
+#pragma unroll
+            for (int k = -R; k <= R; ++k) ldg_p<NP>(cb + (long long)mloc(m0 + k) * M, x[k + R]);
+            if (!mper && (m0 < R || m0 > Nm - 1 - R)) {
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    float2 xp[2 * R + 1];
+#pragma unroll
+                    for (int k = 0; k <= 2 * R; ++k) xp[k] = x[k][p];
+                    fix_ghosts2<R>(xp, m0, Nm);
+#pragma unroll
+                    for (int k = 0; k <= 2 * R; ++k) x[k][p] = xp[k];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < R; ++k)
+#pragma unroll
+                for (int p = 0; p < NP; ++p) win[k][p] = x[R + k][p];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                if constexpr (R == 2) {
+                    dd0[p] = d2p(x[1][p], x[2][p], x[3][p]);
+                    mL[p] = pick2(d2p(x[0][p], x[1][p], x[2][p]), dd0[p]);
+                    dL[p] = sub2(x[2][p], x[1][p]);
+                    if constexpr (!PASS2) inc_val(fma2(f2s(0.5f), mL[p], dL[p]), mn[MA], mx[MA]);   // D-_{m0}
+                } else {
+                    dL[p] = sub2(x[1][p], x[0][p]);
+                    if constexpr (!PASS2) inc_val(dL[p], mn[MA], mx[MA]);
+                }
+            }
+            if (!mper && m1 + R >= Nm) {                 // the segment reaches the high face
+                float2 e[NP], in[NP];
+                ldg_p<NP>(cb + (long long)(Nm - 1 - mlo) * M, e);
+                ldg_p<NP>(cb + (long long)(Nm - 2 - mlo) * M, in);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    gE[p] = e[p];
+                    gS[p] = f2(fabsf(e[p].x - in[p].x) * sgn1(e[p].x), fabsf(e[p].y - in[p].y) * sgn1(e[p].y));
+                }
+            }
+        }
+
+        for (int jg = m0; jg < m1; ++jg, ++it) {
+            const int jl = jg - mlo;
+            const long long gi = U.cbase + (long long)jl * M + grow * N1 + qc0;   // element of node 0
+            // window value entering at this step: v_{j+R} (ring when inside the segment, else global/ghost)
+            const int kin = jg + R;
+            float2 vin[NP];
+            const bool in_ring = kin < m1;
+            if (act && !in_ring) {
+                if (mper || kin < Nm) ldg_p<NP>(cb + (long long)mloc(kin) * M, vin);
+                else {
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) vin[p] = fma2(f2s((float)(kin - Nm + 1)), gS[p], gE[p]);
+                }
+            }
+            float2 vnv[NP], ttv[NP];
+            if constexpr (PASS2) {
+                if (act) {
+                    if (kind == STAGE_RK2) ldg_plain<NP>(Vn + gi, vnv);
+                    if (brt && kind != STAGE_RK1) ldg_p<NP>(T + gi, ttv);
+                }
+            }
+            mbar_wait(&full[it & 1], (uint32_t)((it >> 1) & 1));
+            const float *rc = rbase + rs0 * RSZ;                         // this thread's nodes in the centre tile
+            const float *sb = sbase + (it & 1) * (NSS * SSZ);            // ... in side slot 0
+
+            if (act) {
+                if (in_ring) lds_p<NP>(rbase + (rs0 + R >= RS ? rs0 + R - RS : rs0 + R) * RSZ, vin);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) win[R][p] = vin[p];
+                Pt q0;
+                if constexpr (PASS2) {
+                    q0 = qrow;
+                    load_axis<F>(g, q0, MA, jg);
+                }
+                float2 acc[NP], dis[NP];
+#pragma unroll
+                for (int p = 0; p < NP; ++p) { acc[p] = f2s(0.f); dis[p] = f2s(0.f); }
+                auto qpair = [&](int p, Pt &a0, Pt &a1) {
+                    a0 = q0; a1 = q0;
+                    a0.x[NDIM - 1] = qcv[2 * p].x[NDIM - 1]; a0.c[NDIM - 1] = qcv[2 * p].c[NDIM - 1]; a0.s[NDIM - 1] = qcv[2 * p].s[NDIM - 1];
+                    a1.x[NDIM - 1] = qcv[2 * p + 1].x[NDIM - 1]; a1.c[NDIM - 1] = qcv[2 * p + 1].c[NDIM - 1]; a1.s[NDIM - 1] = qcv[2 * p + 1].s[NDIM - 1];
+                };
+
+                // ---- marching axis: carried edge j-1/2, new edge j+1/2 ----
+                const bool mhi_excl = (R == 2) && !mper && jg == Nm - 1;
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    if constexpr (R == 2) {
+                        const float2 dd1 = d2p(win[0][p], win[1][p], win[2][p]);      // d2_{j+1}
+                        const float2 m = pick2(dd0[p], dd1);
+                        const float2 d1 = sub2(win[1][p], win[0][p]);
+                        if constexpr (PASS2) {
+                            Pt a0, a1;
+                            qpair(p, a0, a1);
+                            axis_terms(f, MA, a0, a1, hih[MA], fma2(f2s(0.5f), mL[p], dL[p]), fma2(f2s(-0.5f), m, d1),
+                                       acc[p], dis[p]);
+                        } else {
+                            if (mhi_excl) inc_val(fma2(f2s(-0.5f), m, d1), mn[MA], mx[MA]);
+                            else inc_edge(m, d1, mn[MA], mx[MA]);
+                        }
+                        dd0[p] = dd1; mL[p] = m; dL[p] = d1;
+                    } else {
+                        const float2 d1 = sub2(win[1][p], win[0][p]);
+                        if constexpr (PASS2) {
+                            Pt a0, a1;
+                            qpair(p, a0, a1);
+                            axis_terms(f, MA, a0, a1, hih[MA], dL[p], d1, acc[p], dis[p]);
+                        } else {
+                            inc_val(d1, mn[MA], mx[MA]);
+                        }
+                        dL[p] = d1;
+                    }
+                }
+
+                // ---- side axes (CTA-uniform faces), neighbours from the side slots ----
+#pragma unroll
+                for (int o = 0; o < MA; ++o) {
+                    float2 sv[2 * R][NP];
+                    const bool full = PASS2 || oface[o];
+#pragma unroll
+                    for (int s2 = 0; s2 < 2 * R; ++s2)
+                        if (full || s2 > 0 || R == 1) lds_p<NP>(sb + (o * 2 * R + s2) * SSZ, sv[s2]);
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+                        if (full) {
+                            float2 x[2 * R + 1];
+#pragma unroll
+                            for (int k = -R; k <= R; ++k) x[k + R] = k == 0 ? win[0][p] : sv[k < 0 ? k + R : k + R - 1][p];
+                            if (oface[o]) fix_ghosts2<R>(x, oid[o], oN[o]);
+                            float2 uu, ww, mr, d1r;
+                            if constexpr (R == 2) {
+                                const float2 dm = d2p(x[0], x[1], x[2]), dc = d2p(x[1], x[2], x[3]), dp = d2p(x[2], x[3], x[4]);
+                                uu = fma2(f2s(0.5f), pick2(dm, dc), sub2(x[2], x[1]));
+                                mr = pick2(dc, dp);
+                                d1r = sub2(x[3], x[2]);
+                                ww = fma2(f2s(-0.5f), mr, d1r);
+                            } else {
+                                uu = sub2(x[1], x[0]);
+                                ww = sub2(x[2], x[1]);
+                                mr = ww; d1r = ww;
+                            }
+                            if constexpr (PASS2) {
+                                Pt a0, a1;
+                                qpair(p, a0, a1);
+                                axis_terms(f, o, a0, a1, hih[o], uu, ww, acc[p], dis[p]);
+                            } else {
+                                inc_val(uu, mn[o], mx[o]);
+                                inc_val(ww, mn[o], mx[o]);
+                                if (R == 2 && oid[o] + 1 <= oN[o] - 1) inc_val(fma2(f2s(0.5f), mr, d1r), mn[o], mx[o]);
+                            }
+                        } else {
+                            // pass 1, interior: the node's upper edge i+1/2 (both sides)
+                            if constexpr (R == 2) {
+                                const float2 dc = d2p(sv[1][p], win[0][p], sv[2][p]);
+                                const float2 dp = d2p(win[0][p], sv[2][p], sv[3][p]);
+                                inc_edge(pick2(dc, dp), sub2(sv[2][p], win[0][p]), mn[o], mx[o]);
+                            } else {
+                                inc_val(sub2(sv[1][p], win[0][p]), mn[o], mx[o]);
+                            }
+                        }
+                    }
+                }
+
+                // ---- in-plane rows (axis n-2) from the centre tile ----
+                {
+                    float2 rv[2 * R][NP];                  // rows -R..-1, +1..+R
+#pragma unroll
+                    for (int k = -R; k <= R; ++k) {
+                        if (k == 0) continue;
+                        if (!PASS2 && R == 2 && k == -2) continue;   // pass 1: rows -1..+2 (+ -2 from ghosts on the face)
+                        lds_p<NP>(rc + k * N1, rv[k < 0 ? k + R : k + R - 1]);
+                    }
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+                        float2 x[2 * R + 1];
+#pragma unroll
+                        for (int k = -R; k <= R; ++k) x[k + R] = k == 0 ? win[0][p] : rv[k < 0 ? k + R : k + R - 1][p];
+                        if constexpr (PASS2) {
+                            if (rlo || rhi) fix_ghosts2<R>(x, grow, N2);
+                            float2 uu, ww;
+                            if constexpr (R == 2) {
+                                const float2 dm = d2p(x[0], x[1], x[2]), dc = d2p(x[1], x[2], x[3]), dp = d2p(x[2], x[3], x[4]);
+                                uu = fma2(f2s(0.5f), pick2(dm, dc), sub2(x[2], x[1]));
+                                ww = fma2(f2s(-0.5f), pick2(dc, dp), sub2(x[3], x[2]));
+                            } else {
+                                uu = sub2(x[1], x[0]);
+                                ww = sub2(x[2], x[1]);
+                            }
+                            Pt a0, a1;
+                            qpair(p, a0, a1);
+                            axis_terms(f, NDIM - 2, a0, a1, hih[NDIM - 2], uu, ww, acc[p], dis[p]);
+                        } else {
+                            if constexpr (R == 2) {
+                                // upper edge r+1/2 from rows r-1..r+2 (x[1..4]); faces in registers
+                                if (rhi) {
+                                    if (grow == N2 - 2) x[4] = ghost2(x[3], x[2], 1.f);
+                                    else { x[3] = ghost2(x[2], x[1], 1.f); x[4] = ghost2(x[2], x[1], 2.f); }
+                                }
+                                if (rlo && grow == 0) x[1] = ghost2(x[2], x[3], 1.f);
+                                const float2 dc = d2p(x[1], x[2], x[3]), dp = d2p(x[2], x[3], x[4]);
+                                const float2 m = pick2(dc, dp), d1 = sub2(x[3], x[2]);
+                                if (rhi && grow == N2 - 1) inc_val(fma2(f2s(-0.5f), m, d1), mn[NDIM - 2], mx[NDIM - 2]);
+                                else inc_edge(m, d1, mn[NDIM - 2], mx[NDIM - 2]);
+                                if (rlo && grow == 0) {            // + D-_0 of the face edge -1/2
+                                    const float2 g2 = ghost2(x[2], x[3], 2.f);
+                                    const float2 dm = d2p(g2, x[1], x[2]);
+                                    inc_val(fma2(f2s(0.5f), pick2(dm, dc), sub2(x[2], x[1])), mn[NDIM - 2], mx[NDIM - 2]);
+                                }
+                            } else {
+                                if (rhi) x[2] = ghost2(x[1], x[0], 1.f);
+                                inc_val(sub2(x[2], x[1]), mn[NDIM - 2], mx[NDIM - 2]);
+                                if (rlo) {                          // D-_0 = v_0 - ghost_{-1}
+                                    x[0] = ghost2(x[1], x[2], 1.f);
+                                    inc_val(sub2(x[1], x[0]), mn[NDIM - 2], mx[NDIM - 2]);
+                                }
+                            }
+                        }
+                    }
+                }
+
+                // ---- in-plane columns (axis n-1): the thread's VEC nodes share interior edges ----
+                {
+                    float c[VEC + 2 * R];                  // columns qc0-R .. qc0+VEC-1+R
+                    {
+                        const float2 lp = *reinterpret_cast<const float2 *>(a.per1 ? rc + loff : rc - 2);
+                        const float2 rp = *reinterpret_cast<const float2 *>(a.per1 ? rc + roff : rc + VEC);
+                        if constexpr (R == 2) { c[0] = lp.x; c[1] = lp.y; } else { c[0] = lp.y; }
+#pragma unroll
+                        for (int p = 0; p < NP; ++p) { c[R + 2 * p] = win[0][p].x; c[R + 2 * p + 1] = win[0][p].y; }
+                        c[R + VEC] = rp.x;
+                        if constexpr (R == 2) c[R + VEC + 1] = rp.y;
+                    }
+                    if (clo) {
+#pragma unroll
+                        for (int k = 1; k <= R; ++k) c[R - k] = ghost(c[R], c[R + 1], (float)k);
+                    }
+                    if (chi) {
+#pragma unroll
+                        for (int k = 1; k <= R; ++k) c[R + VEC - 1 + k] = ghost(c[R + VEC - 1], c[R + VEC - 2], (float)k);
+                    }
+                    // edges e = 0 .. VEC (edge e lies between local columns e-1 and e)
+                    float em[VEC + 1], e1[VEC + 1];
+                    if constexpr (R == 2) {
+                        float d2[VEC + 2];                 // d2 at local columns -1 .. VEC
+#pragma unroll
+                        for (int k = 0; k < VEC + 2; ++k) d2[k] = d2s(c[k], c[k + 1], c[k + 2]);
+#pragma unroll
+                        for (int e = 0; e <= VEC; ++e) { em[e] = pick1(d2[e], d2[e + 1]); e1[e] = c[e + 2] - c[e + 1]; }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e <= VEC; ++e) { em[e] = 0.f; e1[e] = c[e + 1] - c[e]; }
+                    }
+                    if constexpr (PASS2) {
+#pragma unroll
+                        for (int p = 0; p < NP; ++p) {
+                            const int i0 = 2 * p, i1 = 2 * p + 1;   // node i: edges i (left) and i+1 (right)
+                            float2 uu, ww;
+                            if constexpr (R == 2) {
+                                uu = fma2(f2s(0.5f), f2(em[i0], em[i1]), f2(e1[i0], e1[i1]));
+                                ww = fma2(f2s(-0.5f), f2(em[i0 + 1], em[i1 + 1]), f2(e1[i0 + 1], e1[i1 + 1]));
+                            } else {
+                                uu = f2(e1[i0], e1[i1]);
+                                ww = f2(e1[i0 + 1], e1[i1 + 1]);
+                            }
+                            Pt a0, a1;
+                            qpair(p, a0, a1);
+                            axis_terms(f, NDIM - 1, a0, a1, hih[NDIM - 1], uu, ww, acc[p], dis[p]);
+                        }
+                    } else {
+                        float &cmn = mn[NDIM - 1], &cmx = mx[NDIM - 1];
+                        if constexpr (R == 2) {
+                            inc_s(fmaf(0.5f, em[0], e1[0]), cmn, cmx);                 // D- of the first node
+#pragma unroll
+                            for (int e = 1; e + 1 < VEC; e += 2) inc_edge(f2(em[e], em[e + 1]), f2(e1[e], e1[e + 1]), cmn, cmx);
+                            if (chi) {     // last edge: D+ of the last node only
+                                inc_edge(f2(em[VEC - 1], em[VEC - 1]), f2(e1[VEC - 1], e1[VEC - 1]), cmn, cmx);
+                                inc_s(fmaf(-0.5f, em[VEC], e1[VEC]), cmn, cmx);
+                            } else {
+                                inc_edge(f2(em[VEC - 1], em[VEC]), f2(e1[VEC - 1], e1[VEC]), cmn, cmx);
+                            }
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < VEC; e += 2) inc_val(f2(e1[e], e1[e + 1]), cmn, cmx);
+                            inc_s(e1[VEC], cmn, cmx);
+                        }
+                    }
+                }
+
+                if constexpr (PASS2) {
+                    float2 o2[NP];
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+                        const float2 L = add2(ham_fin2(f, acc[p]), dis[p]);
+                        float2 v = fma2(f2s(dt), L, win[0][p]);                 // W + dt L
+                        if (kind == STAGE_RK2) v = mul2(f2s(0.5f), add2(vnv[p], v));   // (Vn + V2)/2 (A10)
+                        if (brt && kind != STAGE_RK1) v = f2(fminf(v.x, ttv[p].x), fminf(v.y, ttv[p].y));
+                        o2[p] = v;
+                    }
+                    st_p<NP>(out + gi, o2);
+                } else {
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) mabs = max3nan(mabs, fabsf(win[0][p].x), fabsf(win[0][p].y));
+                }
+#pragma unroll
+                for (int k = 0; k < R; ++k)
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) win[k][p] = win[k + 1][p];
+            }
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&empty[it & 1]);   // this warp is done with the step's buffers
+            rs0 = rs0 + 1 == RS ? 0 : rs0 + 1;
+        }
+    }
+    if constexpr (!PASS2) {
+#pragma unroll
+        for (int d = 0; d < NDIM; ++d) { mn[d] *= g.inv_dx[d]; mx[d] *= g.inv_dx[d]; }   // h D -> D
+        const int nan = mabs != mabs;
+        block_reduce_range<NDIM>(mn, mx, nan ? 0.f : mabs, nan, partials);
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------------------
+typedef void (*march_fn)(MarchArgs, GridDev, const float *, const float *, const float *, float *, float *,
+                         const DevState *, FParams, int, int);
+
+// The generic (runtime-geometry) instance plus shape-specialised ones for the tile shapes of the
+// BASELINE.json configs (c1 36x(21), c2 60x(15), c3 40x(20), c4 30x(30), c5 48x(16); the row
+// block B in parentheses is what march_plan picks for those shapes).  Any other grid runs the
+// generic instance -- same code, geometry from MarchArgs.
+struct MarchInst {
+    int n1 = 0, b = 0;
+    march_fn pass1 = nullptr, pass2 = nullptr;
+};
+constexpr int MARCH_MAX_INST = 4;
+struct MarchFnsAll {
+    march_fn pass1 = nullptr, pass2 = nullptr;   // generic
+    MarchInst inst[MARCH_MAX_INST];
+    int ninst = 0;
+};
+struct MarchFns {
+    march_fn pass1 = nullptr, pass2 = nullptr;
+    int specialised = 0;
+};
+struct MarchPlan {
+    MarchArgs a;
+    int block = 0, grid = 0;
+    size_t smem = 0;
+};
+
+template <class F, int NDIM, int R, int CN1, int CB>
+void march_add(MarchFnsAll &t) {
+    if constexpr (NDIM >= 3) {
+        MarchInst &m = t.inst[t.ninst++];
+        m.n1 = CN1; m.b = CB;
+        m.pass1 = k_march<F, NDIM, R, 1, false, CN1, CB>;
+        m.pass2 = k_march<F, NDIM, R, 1, true, CN1, CB>;
+    }
+}
+
+template <class F, int NDIM, int R>
+MarchFnsAll march_fns() {
+    MarchFnsAll t;
+    if constexpr (NDIM >= 3) {
+        t.pass1 = k_march<F, NDIM, R, 1, false>;
+        t.pass2 = k_march<F, NDIM, R, 1, true>;
+        if constexpr (std::is_same<F, FDoubleInt6D>::value) {     // c4 (30^6), c5 (64 x 48^5)
+            march_add<F, NDIM, R, 30, 30>(t);
+            march_add<F, NDIM, R, 48, 16>(t);
+        } else if constexpr (std::is_same<F, FCar5D>::value && R == 2) {   // c3
+            march_add<F, NDIM, R, 40, 20>(t);
+        } else if constexpr (std::is_same<F, FCar4D>::value && R == 1) {   // c2
+            march_add<F, NDIM, R, 60, 15>(t);
+        } else if constexpr (std::is_same<F, FDubins3D>::value && R == 1) { // c1
+            march_add<F, NDIM, R, 36, 21>(t);
+        }
+    }
+    return t;
+}
+
+// Whether the march family covers this grid (and the alignment of the arrays it vector-loads).
+inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const void *T, const void *W,
+                       MarchFns *fns, MarchPlan *p) {
+    if (g.n < 3 || !all.pass1) return false;
+    const int N2 = g.N[g.n - 2], N1 = g.N[g.n - 1];
+    const long long M = (long long)N2 * N1;
+    if (N2 < 2 * R + 1 || N1 < 2 * R || N1 % 2) return false;
+    if (M % 4) return false;                                     // tile bases 16-B aligned
+    if (g.per[g.n - 2] && (R * N1) % 4) return false;             // periodic halo rows copied exactly
+    if (T && ((uintptr_t)T % 8)) return false;
+    if ((uintptr_t)W % 16) return false;
+    const int MA = g.n - 3;
+    const int NSS = 2 * R * MA;
+    const int QR = N1 / 2;
+    // rows per block: among the B (B N1 % 4 == 0 unless B = N2, <= 512 threads) whose shared
+    // memory leaves room for 2 CTAs per SM (else 1), the one wasting the fewest rows in the last
+    // (ragged) block, the larger on ties
+    int best = 0;
+    for (int pass = 0; pass < 2 && !best; ++pass) {
+        const int cap = pass == 0 ? 113 * 1024 : 226 * 1024;
+        int best_waste = 1 << 30;
+        for (int B = std::min(N2, (MARCH_MAXT1 - 32) / QR); B >= 1; --B) {
+            if (B != N2 && (B * N1) % 4) continue;
+            if (geo_smem_bytes(R, N1, B, NSS) > cap) continue;
+            const int waste = ((N2 + B - 1) / B) * B - N2;
+            if (waste < best_waste) { best_waste = waste; best = B; }
+        }
+    }
+    if (const char *env = getenv("ODP_MARCH_B")) {
+        const int B = atoi(env);
+        if (B >= 1 && B <= N2 && B * QR + 32 <= MARCH_MAXT1 && (B == N2 || (B * N1) % 4 == 0)) best = B;
+    }
+    if (!best) return false;
+    fns->pass1 = all.pass1;
+    fns->pass2 = all.pass2;
+    fns->specialised = 0;
+    const bool generic_only = getenv("ODP_MARCH_GENERIC") != nullptr;
+    for (int i = 0; i < all.ninst && !generic_only; ++i)
+        if (all.inst[i].n1 == N1 && all.inst[i].b == best) {
+            fns->pass1 = all.inst[i].pass1;
+            fns->pass2 = all.inst[i].pass2;
+            fns->specialised = 1;
+        }
+    MarchArgs &a = p->a;
+    a.M = (int)M; a.N2 = N2; a.N1 = N1;
+    a.per2 = g.per[g.n - 2]; a.per1 = g.per[g.n - 1];
+    a.QR = QR;
+    a.B = best;
+    a.nrb = (N2 + best - 1) / best;
+    a.nthr = best * QR;
+    a.RSZ = geo_rsz(R, N1, best);
+    a.SSZ = geo_ssz(N1, best);
+    a.NSS = NSS;
+    a.rmarg = geo_rmarg(R, N1);
+    a.side_off = geo_side_off(R, N1, best);
+    a.bar_off = geo_bar_off(R, N1, best, NSS);
+    a.tab_off = a.bar_off + 8;
+    const int Nm = g.N[MA];
+    long long ncols = 1;
+    for (int o = 0; o < MA; ++o) ncols *= g.N[o];
+    const long long cols_rb = ncols * a.nrb;
+    a.K = Nm;
+    if (cols_rb < 148LL * 4) a.K = std::max(4, Nm / (int)std::max<long long>(1, (148 * 8) / cols_rb));
+    if (const char *env = getenv("ODP_MARCH_K")) a.K = std::max(1, atoi(env));
+    a.K = std::min(a.K, Nm);
+    a.nseg = (Nm + a.K - 1) / a.K;
+    if (cols_rb * a.nseg > (1LL << 31) - 1) return false;
+    a.units = (int)(cols_rb * a.nseg);
+    p->block = ((a.nthr + 31) / 32) * 32 + 32;      // compute warps + the producer warp
+    p->smem = (size_t)geo_smem_bytes(R, N1, best, NSS);
+    p->grid = 0;
+    return true;
+}
+
+inline int march_prepare(const MarchFns &t, MarchPlan &p, int nsm) {
+    for (march_fn fn : {t.pass1, t.pass2}) {
+        if (cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) != cudaSuccess)
+            return 1;
+    }
+    int occ1 = 0, occ2 = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, (const void *)t.pass1, p.block, p.smem) != cudaSuccess) return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, (const void *)t.pass2, p.block, p.smem) != cudaSuccess) return 1;
+    const int occ = std::max(1, std::min(occ1, occ2));
+    p.grid = std::min(p.a.units, nsm * occ);
+    return 0;
+}
+
+inline void march_pass1(const MarchFns &t, const MarchPlan &p, const GridDev &g, const float *W, float *partials,
+                        const DevState *st, cudaStream_t s) {
+    FParams fp;
+    memset(&fp, 0, sizeof fp);
+    t.pass1<<<p.grid, p.block, p.smem, s>>>(p.a, g, W, nullptr, nullptr, nullptr, partials, st, fp, 0, 0);
+}
+
+inline void march_pass2(const MarchFns &t, const MarchPlan &p, const GridDev &g, const float *W, const float *Vn,
+                        const float *T, float *out, const DevState *st, const FParams &fp, int kind, int brt,
+                        cudaStream_t s) {
+    t.pass2<<<p.grid, p.block, p.smem, s>>>(p.a, g, W, Vn, T, out, nullptr, st, fp, kind, brt);
+}
+
+}  // namespace odp

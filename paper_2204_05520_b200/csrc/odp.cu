@@ -16,7 +16,7 @@
 #include <vector>
 
 #include "../../include/odp.h"
-#include "kernels_stream.cuh"
+#include "kernels_march.cuh"
 
 using namespace odp;
 
@@ -163,6 +163,7 @@ struct KernelSet {
     fin_fn fin = nullptr;
     TiledFns tiled;      // tiled family (may be empty)
     StreamFnsAll stream; // stream family (may be empty)
+    MarchFnsAll march;   // march family (may be empty)
 };
 
 template <class F, int NDIM, int R>
@@ -173,6 +174,7 @@ static KernelSet make_set() {
     k.fin = k_finalize<F, NDIM>;
     k.tiled = tiled_fns<F, NDIM, R>();
     k.stream = stream_fns<F, NDIM, R>();
+    k.march = march_fns<F, NDIM, R>();
     return k;
 }
 
@@ -346,6 +348,7 @@ static GridDev make_griddev(const odp_grid *g) {
         d.Ng[k] = (int)g->N[k];
         d.per[k] = g->per[k];
         d.inv_dx[k] = (float)(1.0 / g->dx[k]);
+        d.hih[k] = 0.5f * d.inv_dx[k];
         d.dx[k] = (float)g->dx[k];
         d.tab_off[k] = g->tab_off[k];
     }
@@ -413,16 +416,26 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
     if ((st = ensure_device(g, std::max(grid_generic, nsm * 8)))) return st;
     GridDev gd = make_griddev(g);
 
-    bool use_stream = false, use_tiled = false;
+    const float *Tcheck = (opts && opts->target) ? opts->target : V0;
+    bool use_march = false, use_stream = false, use_tiled = false;
+    MarchPlan mp;
+    MarchFns mfn;
     StreamPlan sp;
     StreamFns sfn;
     TiledPlan tp;
-    if (want_kernel == ODP_KERNEL_AUTO || want_kernel == ODP_KERNEL_STREAM)
+    if (want_kernel == ODP_KERNEL_AUTO || want_kernel == ODP_KERNEL_MARCH)
+        use_march = march_plan(gd, R, ks.march, Tcheck, g->d_buf[0] + g->halo_elems, &mfn, &mp);
+    if (want_kernel == ODP_KERNEL_MARCH && !use_march) return fail(ODP_EINVAL, "march kernels do not cover this grid");
+    if (!use_march && (want_kernel == ODP_KERNEL_AUTO || want_kernel == ODP_KERNEL_STREAM))
         use_stream = stream_plan(gd, R, ks.stream, &sfn, &sp);
     if (want_kernel == ODP_KERNEL_STREAM && !use_stream) return fail(ODP_EINVAL, "stream kernels do not cover this grid");
-    if (!use_stream && (want_kernel == ODP_KERNEL_AUTO || want_kernel == ODP_KERNEL_TILED) && ks.tiled.pass1)
+    if (!use_march && !use_stream && (want_kernel == ODP_KERNEL_AUTO || want_kernel == ODP_KERNEL_TILED) && ks.tiled.pass1)
         use_tiled = tiled_plan(gd, R, nsm, &tp);
     if (want_kernel == ODP_KERNEL_TILED && !use_tiled) return fail(ODP_EINVAL, "tiled kernels do not cover this grid");
+    if (use_march) {
+        if (march_prepare(mfn, mp, nsm)) return fail(ODP_ECUDA, "march kernel attribute setup failed");
+        if ((st = ensure_device(g, mp.grid))) return st;
+    }
     if (use_stream) {
         if (stream_prepare(sfn, sp, nsm)) return fail(ODP_ECUDA, "stream kernel attribute setup failed");
         if ((st = ensure_device(g, sp.grid))) return st;
@@ -431,7 +444,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
         if (tiled_prepare(ks.tiled, tp, nsm)) return fail(ODP_ECUDA, "tiled kernel attribute setup failed");
         if ((st = ensure_device(g, tp.grid))) return st;
     }
-    const int nparts = use_stream ? sp.grid : (use_tiled ? tp.grid : grid_generic);
+    const int nparts = use_march ? mp.grid : use_stream ? sp.grid : (use_tiled ? tp.grid : grid_generic);
 
     cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
     const double cfl = (opts && opts->cfl > 0.0) ? opts->cfl : (accuracy == ODP_LOW ? 0.8 : 0.5);   // A7
@@ -471,12 +484,14 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
     };
 
     auto launch_pass1 = [&](const float *W) {
-        if (use_stream) stream_pass1(sfn, sp, gd, W, g->d_partials, g->d_state, s);
+        if (use_march) march_pass1(mfn, mp, gd, W, g->d_partials, g->d_state, s);
+        else if (use_stream) stream_pass1(sfn, sp, gd, W, g->d_partials, g->d_state, s);
         else if (use_tiled) tiled_pass1(ks.tiled, tp, gd, W, g->d_partials, g->d_state, s);
         else ks.pass1<<<grid_generic, block, 0, s>>>(gd, W, g->d_partials, g->d_state);
     };
     auto launch_pass2 = [&](const float *W, const float *Vn, float *o, int kind) {
-        if (use_stream) stream_pass2(sfn, sp, gd, W, Vn, T, o, g->d_state, fp, kind, brt, s);
+        if (use_march) march_pass2(mfn, mp, gd, W, Vn, T, o, g->d_state, fp, kind, brt, s);
+        else if (use_stream) stream_pass2(sfn, sp, gd, W, Vn, T, o, g->d_state, fp, kind, brt, s);
         else if (use_tiled) tiled_pass2(ks.tiled, tp, gd, W, Vn, T, o, g->d_state, fp, kind, brt, s);
         else ks.pass2<<<grid_generic, block, 0, s>>>(gd, W, Vn, T, o, g->d_state, fp, kind, brt);
     };

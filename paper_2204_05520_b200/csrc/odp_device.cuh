@@ -26,6 +26,7 @@ struct GridDev {
     long long stride[MAXD];  // element strides (stride[n-1] = 1)
     long long P;             // local points = N[0] * stride[0]
     float inv_dx[MAXD];      // float(1/dx_d)
+    float hih[MAXD];         // 0.5f * inv_dx[d] = 1/(2 dx_d)
     float dx[MAXD];
     const float *tab;        // per axis: x[Ng_d], cos x[Ng_d], sin x[Ng_d] (float32 of float64 values)
     int tab_off[MAXD];       // offset of axis d's x-table in tab; cos at +Ng_d, sin at +2 Ng_d

@@ -15,6 +15,21 @@ def run_gpu(w, V0, kernel="auto", **kw):
     return out.cpu().numpy(), info
 
 
+def covers(w, kernel):
+    """Whether a kernel family covers the workload's grid (the library answers EINVAL otherwise)."""
+    import paper_2204_05520_b200 as odp
+    import torch
+    V0 = torch.zeros(w.N, dtype=torch.float32, device="cuda")
+    w1 = w.__class__(**{**w.__dict__, "tau": (0.0, 1e-9)})
+    try:
+        odp.solve_workload(w1, V0, kernel=kernel)
+    except odp.OdpError as e:
+        if "do not cover" in str(e):
+            return False
+        raise
+    return True
+
+
 def run_oracle(w, V0, **kw):
     import oracle
     return oracle.solve_workload(w, V0=V0, **kw)

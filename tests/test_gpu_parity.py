@@ -7,12 +7,12 @@ import numpy as np
 import pytest
 
 from inputs import CONFIGS, Workload, coarsened, holonomic, make_v0
-from tests.parity_util import (TOL, assert_parity, assert_parity_multistep_medium, assert_parity_one_step, run_gpu,
-                                run_oracle)
+from tests.parity_util import (TOL, assert_parity, assert_parity_multistep_medium, assert_parity_one_step, covers,
+                                run_gpu, run_oracle)
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = ["generic", "tiled", "auto"]
+KERNELS = ["generic", "tiled", "stream", "march", "auto"]
 
 SMALL = [
     # (dynamics, params, N, lo, hi, periodic)
@@ -38,6 +38,8 @@ def test_parity_small(case, acc, mode, kernel):
                  ("random_smooth", len(N)))
     if kernel == "tiled" and (len(N) < 3 or (N[-1] * N[-2]) % 4):
         pytest.skip("tiled family needs dims >= 3 and a tile of 4k floats")
+    if kernel in ("stream", "march") and not covers(w, kernel):
+        pytest.skip(f"{kernel} family does not cover this grid")
     for seed in (None, 0):
         V0 = make_v0(w, seed=seed)
         out, info = run_gpu(w, V0, kernel=kernel)
@@ -80,11 +82,12 @@ def test_kernel_families_agree(acc):
     w = coarsened(CONFIGS["c4"], (12, 10, 12, 10, 12, 10), tau=(0.0, 0.05))
     w = w.__class__(**{**w.__dict__, "accuracy": acc, "cfl": 0.8 if acc == "low" else 0.5})
     V0 = make_v0(w)
-    outs = {k: run_gpu(w, V0, kernel=k)[0] for k in ("generic", "tiled", "stream")}
+    outs = {k: run_gpu(w, V0, kernel=k)[0] for k in ("generic", "tiled", "stream", "march")}
     ref = run_oracle(w, V0)
     for k, o in outs.items():
         assert np.abs(o - ref.out).max() <= 1e-5, k
     assert np.abs(outs["tiled"] - outs["stream"]).max() <= 2e-6
+    assert np.abs(outs["march"] - outs["stream"]).max() <= 1e-5   # H assembled as s (c / 2h) vs ((u + w) / 2h) c
 
 
 def test_numeric_failure_reported():
