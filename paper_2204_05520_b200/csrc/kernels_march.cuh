@@ -260,11 +260,16 @@ struct MarchArgs {
     int B, nrb;           // rows per row block, row blocks per tile
     int nthr;             // B * QR
     int RSZ, SSZ;         // floats per ring / side slot
+    int RGT;              // float offset of the column-ghost table in a ring slot
     int NSS;              // side slots per buffer (2R per side axis)
     int rmarg;            // leading margin of a ring slot (keeps TMA destinations 16-B aligned)
     int side_off;         // float offset of the side buffers
     int bar_off;          // float offset of the mbarriers
     int tab_off;          // float offset of the per-unit copy table
+    int sn[3];            // local extents of the side axes (work order, march_col)
+    int b1;               // axis-1 block of the work order (divides sn[1])
+    int ncols;            // columns (product of the side extents)
+    int dbg;              // experiments only (ODP_MARCH_DBG): 1 = skip the data waits, 2 = skip the arithmetic
     int K, nseg, units;   // marching segment length, segments per column, work units
 };
 constexpr int MARCH_SMARG = 4;   // leading margin of a side slot (floats)
@@ -273,17 +278,19 @@ constexpr int MARCH_SMARG = 4;   // leading margin of a side slot (floats)
 // plan and -- for the shape-specialised instances -- as compile-time constants in the kernel, so
 // every stencil read is an LDS at an immediate offset from one per-thread base register.
 __host__ __device__ constexpr int geo_rmarg(int R, int N1) { return 4 + ((-R * N1) & 3); }
-__host__ __device__ constexpr int geo_rsz(int R, int N1, int B) {
+// ring slot: [rmarg][(B + 2R) rows x N1][slack][column-ghost table: (B + 2R) rows x 4 floats]
+__host__ __device__ constexpr int geo_rgt(int R, int N1, int B) {
     return ((geo_rmarg(R, N1) + (B + 2 * R) * N1 + 4 + 3) / 4) * 4;
 }
+__host__ __device__ constexpr int geo_rsz(int R, int N1, int B) { return geo_rgt(R, N1, B) + 4 * (B + 2 * R); }
 __host__ __device__ constexpr int geo_ssz(int N1, int B) { return ((MARCH_SMARG + B * N1 + 3) / 4) * 4; }
 __host__ __device__ constexpr int geo_side_off(int R, int N1, int B) { return (R + 2) * geo_rsz(R, N1, B); }
 __host__ __device__ constexpr int geo_bar_off(int R, int N1, int B, int NSS) {
     return ((geo_side_off(R, N1, B) + 2 * NSS * geo_ssz(N1, B)) + 3) / 4 * 4;
 }
-// 4 mbarriers (32 B) + copy table: 32 x 8 B offsets + 32 x 4 B sizes + 8 x 4 B ring fields
+// 6 mbarriers (48 B, padded to 64) + copy table: 32 x 8 B offsets + 32 x 4 B sizes + 8 x 4 B ring fields
 __host__ __device__ constexpr int geo_smem_bytes(int R, int N1, int B, int NSS) {
-    return geo_bar_off(R, N1, B, NSS) * 4 + 32 + 32 * 8 + 32 * 4 + 8 * 4;
+    return geo_bar_off(R, N1, B, NSS) * 4 + 64 + 32 * 8 + 32 * 4 + 8 * 4;
 }
 
 struct MarchUnit {
@@ -292,12 +299,38 @@ struct MarchUnit {
     long long cbase;              // element offset of the column's tile at local marching index 0
 };
 
+// Work order of the columns (L2 reuse).  A column's side neighbours are the columns at +-1, +-2 on
+// each side axis; CTAs run ~2 x 148 consecutive units at a time, so consecutive units should be
+// side-axis neighbours: axis 0 (the largest stride) varies fastest, then -- for three side axes --
+// axis 2 inside blocks of b1 consecutive axis-1 indices, so the +-2 neighbourhood of a wave stays
+// resident in the 126 MB L2 instead of being re-read from HBM (ncu: 5.2x algorithmic DRAM bytes
+// with the memory order).  Returns the memory-order column index.
+template <int MA>
+__device__ __forceinline__ int march_col(const MarchArgs &a, int c) {
+    if constexpr (MA <= 1) {
+        return c;
+    } else if constexpr (MA == 2) {
+        const int i0 = c % a.sn[0], i1 = c / a.sn[0];
+        return i0 * a.sn[1] + i1;
+    } else {
+        const int i0 = c % a.sn[0];
+        int r = c / a.sn[0];
+        const int i1l = r % a.b1;
+        r /= a.b1;
+        const int i2 = r % a.sn[2];
+        const int i1 = (r / a.sn[2]) * a.b1 + i1l;
+        return (i0 * a.sn[1] + i1) * a.sn[2] + i2;
+    }
+}
+
+template <int MA>
 __device__ __forceinline__ MarchUnit march_unit(const MarchArgs &a, int Nml, int mlo, int u) {
     MarchUnit U;
     const int rb = u % a.nrb;
     const int cs = u / a.nrb;
-    U.col = cs / a.nseg;
-    U.seg = cs - U.col * a.nseg;
+    U.seg = cs / a.ncols;                          // segments slowest: a wave spans many columns, few steps
+    const int c = cs - U.seg * a.ncols;
+    U.col = march_col<MA>(a, c);
     U.rb = rb;
     U.r0 = rb * a.B;
     U.nrow = min(a.B, a.N2 - U.r0);
@@ -307,27 +340,52 @@ __device__ __forceinline__ MarchUnit march_unit(const MarchArgs &a, int Nml, int
     return U;
 }
 
+// mbarrier wait with back-off: a warp that finds its data missing sleeps instead of spinning, so
+// it does not take issue slots from the warps that are computing
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    while (!ok) {
+        __nanosleep(64);
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    }
+}
+
 template <class F, int NDIM, int R, int NP, bool PASS2, int CN1 = 0, int CB = 0>
-__global__ void __launch_bounds__(NP == 1 ? MARCH_MAXT1 : MARCH_MAXT2, NP == 1 ? ODP_MARCH_MINB1 : ODP_MARCH_MINB2)
+__global__ void __launch_bounds__(MARCH_MAXT1, ODP_MARCH_MINB1)
 k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, const float *__restrict__ T,
         float *out, float *partials, const DevState *st, FParams fp, int kind, int brt) {
+    static_assert(NP == 1, "the march family computes node pairs (VEC = 2)");
     if (!st->active) return;
-    constexpr int VEC = 2 * NP;
+    constexpr int VEC = 2;
     constexpr int NO = NDIM - 2;     // outer axes
     constexpr int MA = NO - 1;       // marching axis; axes 0..MA-1 are the side axes
     constexpr int NSA = MA > 0 ? MA : 1;
     constexpr int RS = R + 2;        // ring slots
     constexpr bool CT = CN1 > 0;     // shape-specialised instance: geometry known at compile time
-    constexpr int NSS_CT = 2 * R * MA;
+    constexpr int NSS = 2 * R * MA;  // side slots per stage
     extern __shared__ __align__(128) float smem[];
     const int N1 = CT ? CN1 : a.N1;
     const int RSZ = CT ? geo_rsz(R, CN1, CB) : a.RSZ;
+    const int RGT = CT ? geo_rgt(R, CN1, CB) : a.RGT;
     const int SSZ = CT ? geo_ssz(CN1, CB) : a.SSZ;
     const int RMG = CT ? geo_rmarg(R, CN1) : a.rmarg;
-    const int NSS = NSS_CT;
     float *ring = smem;
     float *side = smem + (CT ? geo_side_off(R, CN1, CB) : a.side_off);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + a.bar_off);
+    // tma[b]:   the copies of a step with parity b landed (producer arrive.expect_tx + bytes)
+    // empty[b]: every compute warp is done reading that step's buffers (one arrive per warp)
+    // gh[k]:    the ghost cells of the centre tile in ring slot k are written (producer arrive);
+    //           filled as soon as the tile lands, R steps before it becomes a centre tile
+    uint64_t *tmab = bars, *empty = bars + 2, *gh = bars + 4;
 
     float mn[NDIM], mx[NDIM], mabs = 0.f;
 #pragma unroll
@@ -343,13 +401,14 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     const int N2 = a.N2, M = a.M;
     const int QR = N1 / VEC;
     const int tid = threadIdx.x;
+    const int nwc = (a.nthr + 31) >> 5;                // compute warps; warp nwc is the producer
     const int lrow = tid / QR;                         // row within the row block
     const int qc0 = (tid - lrow * QR) * VEC;           // first column of this thread's nodes
-    const int loff = (a.per1 && qc0 == 0) ? N1 - 2 : -2;              // left pair (cols c0-2, c0-1)
-    const int roff = (a.per1 && qc0 + VEC == N1) ? VEC - N1 : VEC;    // right pair (cols c0+VEC, +1)
-    const bool clo = !a.per1 && qc0 == 0, chi = !a.per1 && qc0 + VEC == N1;
     const int toff = RMG + (lrow + R) * N1 + qc0;      // this thread's nodes in a ring slot
     const int sloc = MARCH_SMARG + lrow * N1 + qc0;    // ... in a side slot
+    // left / right column pairs: the tile itself, or the slot's column-ghost table on the faces
+    const int loff = qc0 == 0 ? RGT + (lrow + R) * 4 - toff : -2;
+    const int roff = qc0 + VEC == N1 ? RGT + (lrow + R) * 4 + 2 - toff : VEC;
     Pt qcv[VEC];                                       // in-plane column coordinates (pass 2)
     if constexpr (PASS2) {
 #pragma unroll
@@ -368,7 +427,6 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
         }
         return j - mlo;
     };
-    // side-axis geometry of a column: global index and extent per side axis
     auto side_geom = [&](int col, int *oid, int *oN) {
         int r = col;
 #pragma unroll
@@ -376,13 +434,10 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
         if constexpr (MA >= 1) { oid[0] = g.g0 + r; oN[0] = g.Ng0; }
     };
 
-    // ---- copy issue (warp 0) ----
-    // Per unit, warp 0 fills a table of the unit's copies (lane l < NSS: side slot l; lane NSS:
-    // the ring tile).  Step j of the unit then needs: side slot l <- tile(j) + soff[l]; ring slot
-    // <- tile(j + R) (or, at the unit's first step, tiles j .. j + R).
+    // ---- producer: copy table of a unit (lane l < NSS: side slot l; lane NSS: the ring tile) ----
     long long *t_soff = reinterpret_cast<long long *>(smem + a.tab_off);   // [32]
     uint32_t *t_snb = reinterpret_cast<uint32_t *>(t_soff + 32);           // [32] bytes (0 = skip)
-    int *t_ring = reinterpret_cast<int *>(t_snb + 32);                      // [8]: fa, nbytes, dst0, wrap-lo bytes, wrap-hi bytes, wrap-hi dst
+    int *t_ring = reinterpret_cast<int *>(t_snb + 32);                      // [8]
     auto make_table = [&](const MarchUnit &U) {
         const int lane = tid & 31;
         int oid[NSA], oN[NSA];
@@ -413,7 +468,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
             fa &= ~3; fb = (fb + 3) & ~3;                              // 16-B granules inside the tile
             t_ring[0] = fa;
             t_ring[1] = (fb - fa) * 4;
-            t_ring[2] = RMG + fa - va * N1;                        // destination float offset in the slot
+            t_ring[2] = RMG + fa - va * N1;                            // destination float offset in the slot
             t_ring[3] = (a.per2 && va < 0) ? (-va) * N1 * 4 : 0;
             t_ring[4] = (a.per2 && vb > N2) ? (vb - N2) * N1 * 4 : 0;
             t_ring[5] = RMG + (N2 - va) * N1;
@@ -421,10 +476,10 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
         }
         __syncwarp();
     };
-    // copies of step `itx` = marching index j of unit U (ring tiles j+kb .. j+R)
+    // copies of step `itx` = marching index j of unit U (ring tiles j+kb .. j+R), on tma[itx & 1]
     auto issue = [&](const MarchUnit &U, int j, int itx, int kb) {
         const int lane = tid & 31;
-        uint64_t *bar = &bars[itx & 1];
+        uint64_t *bar = &tmab[itx & 1];
         const long long tj = U.cbase + (long long)(j - mlo) * M;
         uint32_t nb = 0, nbw0 = 0, nbw1 = 0;
         const float *src = nullptr;
@@ -454,206 +509,235 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
         if (nbw0) tma_bulk_g2s_u32(smem_u32(slot + RMG), W + tt + t_ring[6], nbw0, bar);
         if (nbw1) tma_bulk_g2s_u32(smem_u32(slot + t_ring[5]), W + tt, nbw1, bar);
     };
+    // ghost cells (A12) of the centre tile of a step, in its ring slot: the extrapolated rows
+    // beyond a non-periodic row face, and per owned row the column table [c-2, c-1 | c+N1, c+N1+1]
+    // (extrapolated, or wrapped copies on a periodic column axis)
+    auto fill_ghosts = [&](const MarchUnit &U, int slotk) {
+        const int lane = tid & 31;
+        float *slot = ring + slotk * RSZ;
+        float *row0 = slot + RMG + R * N1;                      // row r0 of the block
+        if (!a.per2) {
+            // rows below 0 (only when the block starts within R of the face) and above N2 - 1;
+            // one lane per column, all ghost rows of that column
+            const bool lo = U.r0 - R < 0, hi = U.r0 + U.nrow + R > N2;
+            if (lo || hi) {
+                for (int c = lane; c < N1; c += 32) {
+                    if (lo) {
+                        const float e = row0[(0 - U.r0) * N1 + c], in = row0[(1 - U.r0) * N1 + c];
+#pragma unroll
+                        for (int k = 1; k <= R; ++k)
+                            if (-k >= U.r0 - R) row0[(-k - U.r0) * N1 + c] = ghost(e, in, (float)k);
+                    }
+                    if (hi) {
+                        const float e = row0[(N2 - 1 - U.r0) * N1 + c], in = row0[(N2 - 2 - U.r0) * N1 + c];
+#pragma unroll
+                        for (int k = 1; k <= R; ++k)
+                            if (N2 - 1 + k < U.r0 + U.nrow + R) row0[(N2 - 1 + k - U.r0) * N1 + c] = ghost(e, in, (float)k);
+                    }
+                }
+            }
+        }
+        // column table: one lane per owned row: [c-2, c-1 | c+N1, c+N1+1]
+        float *gt = slot + RGT + R * 4;                          // table row of block row 0
+        for (int rr = lane; rr < U.nrow; rr += 32) {
+            const float *rowp = row0 + rr * N1;
+            const float2 l = *reinterpret_cast<const float2 *>(rowp);
+            const float2 h = *reinterpret_cast<const float2 *>(rowp + N1 - 2);
+            float4 t;
+            if (a.per1) t = make_float4(h.x, h.y, l.x, l.y);
+            else t = make_float4(ghost(l.x, l.y, 2.f), ghost(l.x, l.y, 1.f), ghost(h.y, h.x, 1.f), ghost(h.y, h.x, 2.f));
+            *reinterpret_cast<float4 *>(gt + rr * 4) = t;
+        }
+    };
 
-    // ---- warp roles: warps [0, nwc) compute, warp nwc issues the copies (producer) ----
-    // full[b]: the copies of a step with parity b landed (producer arrive + tx bytes);
-    // empty[b]: every compute warp finished reading that step's buffers (one arrive per warp).
-    const int nwc = (a.nthr + 31) >> 5;
-    uint64_t *full = bars, *empty = bars + 2;
     if (tid == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-        mbar_init(&empty[0], nwc);
-        mbar_init(&empty[1], nwc);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tmab[b], 1);
+            mbar_init(&empty[b], nwc);
+        }
+        for (int k = 0; k < RS; ++k) mbar_init(&gh[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if ((tid >> 5) == nwc) {                        // producer warp
-        int sp = 0;
+    if ((tid >> 5) == nwc) {
+        // ================= producer warp =================
+        // iteration s: (b) once step s-1 is released by every compute warp, issue the copies of
+        //                  step s+1 (the TMA latency overlaps step s);
+        //              (a) when step s's copies have landed, write the ghost cells of the ring
+        //                  tiles that came with them (centre tiles R steps later; at a unit's first
+        //                  step all R+1) and release them (gh)
+        int u = blockIdx.x;
+        MarchUnit U = march_unit<MA>(a, Nml, mlo, u);
+        int jg = U.m0;
+        bool first = true;                                   // step sp is the first of its unit
+        make_table(U);
+        issue(U, jg, 0, 0);
+        for (int sp = 0;; ++sp) {
+            int jn = jg + 1, un = u;
+            MarchUnit Un = U;
+            const bool fresh = jn >= U.m1;
+            bool more = true;
+            if (fresh) {
+                un = u + gridDim.x;
+                more = un < a.units;
+                if (more) { Un = march_unit<MA>(a, Nml, mlo, un); jn = Un.m0; }
+            }
+            if (more) {
+                if (sp >= 1) mbar_wait_sleep(&empty[(sp - 1) & 1], (uint32_t)(((sp - 1) >> 1) & 1));
+                if (fresh) make_table(Un);
+                issue(Un, jn, sp + 1, fresh ? 0 : R);
+            }
+            mbar_wait_sleep(&tmab[sp & 1], (uint32_t)((sp >> 1) & 1));
+#pragma unroll 1
+            for (int k = first ? 0 : R; k <= R; ++k) {
+                if (jg + k >= U.m1) break;
+                fill_ghosts(U, (sp + k) % RS);
+                __syncwarp();
+                if ((tid & 31) == 0) mbar_arrive(&gh[(sp + k) % RS]);
+            }
+            if (!more) break;
+            u = un; U = Un; jg = jn; first = fresh;
+        }
+    } else {
+        // ================= compute warps =================
+        int it = 0;                                      // step counter of this CTA (buffer / phase)
+        int rs0 = 0;                                     // it % RS: ring slot of the current centre tile
+        const float *rbase = ring + toff;
+        const float *sbase = side + sloc;
         for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-            const MarchUnit U = march_unit(a, Nml, mlo, u);
-            make_table(U);
-            for (int jg = U.m0; jg < U.m1; ++jg, ++sp) {
-                if (sp >= 2) mbar_wait(&empty[sp & 1], (uint32_t)(((sp >> 1) & 1) ^ 1));
-                issue(U, jg, sp, jg == U.m0 ? 0 : R);
+            const MarchUnit U = march_unit<MA>(a, Nml, mlo, u);
+            const int m0 = U.m0, m1 = U.m1;
+            const bool act = lrow < U.nrow && tid < a.nthr;
+            const int grow = U.r0 + lrow;                 // global row of this thread
+            int oid[NSA], oN[NSA];
+            side_geom(U.col, oid, oN);
+            bool oface[NSA];
+#pragma unroll
+            for (int o = 0; o < MA; ++o) oface[o] = !g.per[o] && (oid[o] < R || oid[o] > oN[o] - 1 - R);
+            Pt qrow;
+            if constexpr (PASS2) {
+#pragma unroll
+                for (int o = 0; o < MA; ++o) load_axis<F>(g, qrow, o, oid[o]);
+                load_axis<F>(g, qrow, NDIM - 2, min(grow, N2 - 1));
             }
-        }
-    }
+            const float *cb = W + U.cbase + grow * N1 + qc0;   // this thread's nodes at local marching index 0
 
-    int it = 0;                                      // step counter of this CTA (buffer / phase)
-    int rs0 = 0;                                     // it % RS: ring slot of the current centre tile
-    const float *rbase = ring + toff;
-    const float *sbase = side + sloc;
-    for (int u = blockIdx.x; u < a.units && (tid >> 5) < nwc; u += gridDim.x) {
-        const MarchUnit U = march_unit(a, Nml, mlo, u);
-        const int m0 = U.m0, m1 = U.m1;
-        const bool act = lrow < U.nrow && tid < a.nthr;
-        const int grow = U.r0 + lrow;                 // global row of this thread
-        const bool rlo = !a.per2 && grow < R, rhi = !a.per2 && grow > N2 - 1 - R;
-        int oid[NSA], oN[NSA];
-        side_geom(U.col, oid, oN);
-        bool oface[NSA];
+            // ---- preamble: the window around m0 and the carried edge m0 - 1/2 (registers) ----
+            float2 win[R + 1];
+            float2 dd0, mL, dL;
+            if (act) {
+                float2 x[2 * R + 1];
 #pragma unroll
-        for (int o = 0; o < MA; ++o) oface[o] = !g.per[o] && (oid[o] < R || oid[o] > oN[o] - 1 - R);
-        Pt qrow;
-        if constexpr (PASS2) {
+                for (int k = -R; k <= R; ++k) x[k + R] = __ldg(reinterpret_cast<const float2 *>(cb + (long long)mloc(m0 + k) * M));
+                if (!mper && (m0 < R || m0 > Nm - 1 - R)) fix_ghosts2<R>(x, m0, Nm);
 #pragma unroll
-            for (int o = 0; o < MA; ++o) load_axis<F>(g, qrow, o, oid[o]);
-            load_axis<F>(g, qrow, NDIM - 2, min(grow, N2 - 1));
-        }
-        const float *cb = W + U.cbase + grow * N1 + qc0;   // this thread's nodes at local marching index 0
-
-        // ---- preamble: the window around m0 and the carried edge m0 - 1/2 (registers) ----
-        float2 win[R + 1][NP];
-        float2 dd0[NP], mL[NP], dL[NP], gE[NP], gS[NP];
-        if (act) {
-            float2 x[2 * R + 1][NP];
-#pragma unroll
-            for (int k = -R; k <= R; ++k) ldg_p<NP>(cb + (long long)mloc(m0 + k) * M, x[k + R]);
-            if (!mper && (m0 < R || m0 > Nm - 1 - R)) {
-#pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                    float2 xp[2 * R + 1];
-#pragma unroll
-                    for (int k = 0; k <= 2 * R; ++k) xp[k] = x[k][p];
-                    fix_ghosts2<R>(xp, m0, Nm);
-#pragma unroll
-                    for (int k = 0; k <= 2 * R; ++k) x[k][p] = xp[k];
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < R; ++k)
-#pragma unroll
-                for (int p = 0; p < NP; ++p) win[k][p] = x[R + k][p];
-#pragma unroll
-            for (int p = 0; p < NP; ++p) {
+                for (int k = 0; k < R; ++k) win[k] = x[R + k];
                 if constexpr (R == 2) {
-                    dd0[p] = d2p(x[1][p], x[2][p], x[3][p]);
-                    mL[p] = pick2(d2p(x[0][p], x[1][p], x[2][p]), dd0[p]);
-                    dL[p] = sub2(x[2][p], x[1][p]);
-                    if constexpr (!PASS2) inc_val(fma2(f2s(0.5f), mL[p], dL[p]), mn[MA], mx[MA]);   // D-_{m0}
+                    dd0 = d2p(x[1], x[2], x[3]);
+                    mL = pick2(d2p(x[0], x[1], x[2]), dd0);
+                    dL = sub2(x[2], x[1]);
+                    if constexpr (!PASS2) inc_val(fma2(f2s(0.5f), mL, dL), mn[MA], mx[MA]);   // D-_{m0}
                 } else {
-                    dL[p] = sub2(x[1][p], x[0][p]);
-                    if constexpr (!PASS2) inc_val(dL[p], mn[MA], mx[MA]);
+                    dL = sub2(x[1], x[0]);
+                    if constexpr (!PASS2) inc_val(dL, mn[MA], mx[MA]);
                 }
             }
-            if (!mper && m1 + R >= Nm) {                 // the segment reaches the high face
-                float2 e[NP], in[NP];
-                ldg_p<NP>(cb + (long long)(Nm - 1 - mlo) * M, e);
-                ldg_p<NP>(cb + (long long)(Nm - 2 - mlo) * M, in);
-#pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                    gE[p] = e[p];
-                    gS[p] = f2(fabsf(e[p].x - in[p].x) * sgn1(e[p].x), fabsf(e[p].y - in[p].y) * sgn1(e[p].y));
-                }
-            }
-        }
-
-        for (int jg = m0; jg < m1; ++jg, ++it) {
-            const int jl = jg - mlo;
-            const long long gi = U.cbase + (long long)jl * M + grow * N1 + qc0;   // element of node 0
-            // window value entering at this step: v_{j+R} (ring when inside the segment, else global/ghost)
-            const int kin = jg + R;
-            float2 vin[NP];
-            const bool in_ring = kin < m1;
-            if (act && !in_ring) {
-                if (mper || kin < Nm) ldg_p<NP>(cb + (long long)mloc(kin) * M, vin);
-                else {
-#pragma unroll
-                    for (int p = 0; p < NP; ++p) vin[p] = fma2(f2s((float)(kin - Nm + 1)), gS[p], gE[p]);
-                }
-            }
-            float2 vnv[NP], ttv[NP];
+            float2 vnv = f2s(0.f), ttv = f2s(0.f);         // Vn / target of the current step (pass 2), loaded a step ahead
             if constexpr (PASS2) {
                 if (act) {
-                    if (kind == STAGE_RK2) ldg_plain<NP>(Vn + gi, vnv);
-                    if (brt && kind != STAGE_RK1) ldg_p<NP>(T + gi, ttv);
+                    const long long gi0 = U.cbase + (long long)(m0 - mlo) * M + grow * N1 + qc0;
+                    if (kind == STAGE_RK2) vnv = *reinterpret_cast<const float2 *>(Vn + gi0);
+                    if (brt && kind != STAGE_RK1) ttv = __ldg(reinterpret_cast<const float2 *>(T + gi0));
                 }
             }
-            mbar_wait(&full[it & 1], (uint32_t)((it >> 1) & 1));
-            const float *rc = rbase + rs0 * RSZ;                         // this thread's nodes in the centre tile
-            const float *sb = sbase + (it & 1) * (NSS * SSZ);            // ... in side slot 0
 
-            if (act) {
-                if (in_ring) lds_p<NP>(rbase + (rs0 + R >= RS ? rs0 + R - RS : rs0 + R) * RSZ, vin);
-#pragma unroll
-                for (int p = 0; p < NP; ++p) win[R][p] = vin[p];
-                Pt q0;
-                if constexpr (PASS2) {
-                    q0 = qrow;
-                    load_axis<F>(g, q0, MA, jg);
-                }
-                float2 acc[NP], dis[NP];
-#pragma unroll
-                for (int p = 0; p < NP; ++p) { acc[p] = f2s(0.f); dis[p] = f2s(0.f); }
-                auto qpair = [&](int p, Pt &a0, Pt &a1) {
-                    a0 = q0; a1 = q0;
-                    a0.x[NDIM - 1] = qcv[2 * p].x[NDIM - 1]; a0.c[NDIM - 1] = qcv[2 * p].c[NDIM - 1]; a0.s[NDIM - 1] = qcv[2 * p].s[NDIM - 1];
-                    a1.x[NDIM - 1] = qcv[2 * p + 1].x[NDIM - 1]; a1.c[NDIM - 1] = qcv[2 * p + 1].c[NDIM - 1]; a1.s[NDIM - 1] = qcv[2 * p + 1].s[NDIM - 1];
-                };
-
-                // ---- marching axis: carried edge j-1/2, new edge j+1/2 ----
-                const bool mhi_excl = (R == 2) && !mper && jg == Nm - 1;
-#pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                    if constexpr (R == 2) {
-                        const float2 dd1 = d2p(win[0][p], win[1][p], win[2][p]);      // d2_{j+1}
-                        const float2 m = pick2(dd0[p], dd1);
-                        const float2 d1 = sub2(win[1][p], win[0][p]);
-                        if constexpr (PASS2) {
-                            Pt a0, a1;
-                            qpair(p, a0, a1);
-                            axis_terms(f, MA, a0, a1, hih[MA], fma2(f2s(0.5f), mL[p], dL[p]), fma2(f2s(-0.5f), m, d1),
-                                       acc[p], dis[p]);
-                        } else {
-                            if (mhi_excl) inc_val(fma2(f2s(-0.5f), m, d1), mn[MA], mx[MA]);
-                            else inc_edge(m, d1, mn[MA], mx[MA]);
-                        }
-                        dd0[p] = dd1; mL[p] = m; dL[p] = d1;
-                    } else {
-                        const float2 d1 = sub2(win[1][p], win[0][p]);
-                        if constexpr (PASS2) {
-                            Pt a0, a1;
-                            qpair(p, a0, a1);
-                            axis_terms(f, MA, a0, a1, hih[MA], dL[p], d1, acc[p], dis[p]);
-                        } else {
-                            inc_val(d1, mn[MA], mx[MA]);
-                        }
-                        dL[p] = d1;
+            for (int jg = m0; jg < m1; ++jg, ++it) {
+                const int jl = jg - mlo;
+                const long long gi = U.cbase + (long long)jl * M + grow * N1 + qc0;   // element of node 0
+                // window value entering at this step: v_{j+R} (ring inside the segment, else global / ghost)
+                const int kin = jg + R;
+                const bool in_ring = kin < m1;
+                float2 vin = f2s(0.f);
+                if (act && !in_ring) {
+                    if (mper || kin < Nm) {
+                        vin = __ldg(reinterpret_cast<const float2 *>(cb + (long long)mloc(kin) * M));
+                    } else {                                  // beyond the high face: ghost (A12)
+                        const float2 e = __ldg(reinterpret_cast<const float2 *>(cb + (long long)(Nm - 1 - mlo) * M));
+                        const float2 in = __ldg(reinterpret_cast<const float2 *>(cb + (long long)(Nm - 2 - mlo) * M));
+                        vin = ghost2(e, in, (float)(kin - Nm + 1));
                     }
                 }
+                if (!(a.dbg & 1)) {
+                    mbar_wait_sleep(&gh[rs0], (uint32_t)((it / RS) & 1));
+                    mbar_wait_sleep(&tmab[it & 1], (uint32_t)((it >> 1) & 1));
+                }
+                const float *rc = rbase + rs0 * RSZ;                         // this thread's nodes in the centre tile
+                const float *sb = sbase + (it & 1) * (NSS * SSZ);            // ... in side slot 0
 
-                // ---- side axes (CTA-uniform faces), neighbours from the side slots ----
+                if (act && !(a.dbg & 2)) {
+                    if (in_ring) vin = *reinterpret_cast<const float2 *>(rbase + (rs0 + R >= RS ? rs0 + R - RS : rs0 + R) * RSZ);
+                    win[R] = vin;
+                    const float2 v0 = win[0];
+                    Pt q0;
+                    if constexpr (PASS2) {
+                        q0 = qrow;
+                        load_axis<F>(g, q0, MA, jg);
+                    }
+                    float2 acc = f2s(0.f), dis = f2s(0.f);
+                    auto terms = [&](int d, float2 uu, float2 ww) {
+                        Pt a0 = q0, a1 = q0;
+                        a0.x[NDIM - 1] = qcv[0].x[NDIM - 1]; a0.c[NDIM - 1] = qcv[0].c[NDIM - 1]; a0.s[NDIM - 1] = qcv[0].s[NDIM - 1];
+                        a1.x[NDIM - 1] = qcv[1].x[NDIM - 1]; a1.c[NDIM - 1] = qcv[1].c[NDIM - 1]; a1.s[NDIM - 1] = qcv[1].s[NDIM - 1];
+                        axis_terms(f, d, a0, a1, hih[d], uu, ww, acc, dis);
+                    };
+                    // one-sided derivatives of a full window x[0..2R] (classic): h D-, h D+
+                    auto classic = [&](const float2 *x, float2 &uu, float2 &ww, float2 &mr, float2 &d1r) {
+                        if constexpr (R == 2) {
+                            const float2 dm = d2p(x[0], x[1], x[2]), dc = d2p(x[1], x[2], x[3]), dp = d2p(x[2], x[3], x[4]);
+                            uu = fma2(f2s(0.5f), pick2(dm, dc), sub2(x[2], x[1]));
+                            mr = pick2(dc, dp);
+                            d1r = sub2(x[3], x[2]);
+                            ww = fma2(f2s(-0.5f), mr, d1r);
+                        } else {
+                            uu = sub2(x[1], x[0]);
+                            ww = sub2(x[2], x[1]);
+                            mr = ww; d1r = ww;
+                        }
+                    };
+
+                    // ---- marching axis: carried edge j-1/2, new edge j+1/2 ----
+                    if constexpr (R == 2) {
+                        const float2 dd1 = d2p(win[0], win[1], win[2]);      // d2_{j+1}
+                        const float2 m = pick2(dd0, dd1);
+                        const float2 d1 = sub2(win[1], win[0]);
+                        if constexpr (PASS2) {
+                            terms(MA, fma2(f2s(0.5f), mL, dL), fma2(f2s(-0.5f), m, d1));
+                        } else {
+                            if (!mper && jg == Nm - 1) inc_val(fma2(f2s(-0.5f), m, d1), mn[MA], mx[MA]);
+                            else inc_edge(m, d1, mn[MA], mx[MA]);
+                        }
+                        dd0 = dd1; mL = m; dL = d1;
+                    } else {
+                        const float2 d1 = sub2(win[1], win[0]);
+                        if constexpr (PASS2) terms(MA, dL, d1);
+                        else inc_val(d1, mn[MA], mx[MA]);
+                        dL = d1;
+                    }
+
+                    // ---- side axes (CTA-uniform faces), neighbours from the side slots ----
 #pragma unroll
-                for (int o = 0; o < MA; ++o) {
-                    float2 sv[2 * R][NP];
-                    const bool full = PASS2 || oface[o];
-#pragma unroll
-                    for (int s2 = 0; s2 < 2 * R; ++s2)
-                        if (full || s2 > 0 || R == 1) lds_p<NP>(sb + (o * 2 * R + s2) * SSZ, sv[s2]);
-#pragma unroll
-                    for (int p = 0; p < NP; ++p) {
-                        if (full) {
+                    for (int o = 0; o < MA; ++o) {
+                        const float *so = sb + (o * 2 * R) * SSZ;
+                        if (PASS2 || oface[o]) {
                             float2 x[2 * R + 1];
 #pragma unroll
-                            for (int k = -R; k <= R; ++k) x[k + R] = k == 0 ? win[0][p] : sv[k < 0 ? k + R : k + R - 1][p];
+                            for (int k = -R; k <= R; ++k)
+                                x[k + R] = k == 0 ? v0 : *reinterpret_cast<const float2 *>(so + (k < 0 ? k + R : k + R - 1) * SSZ);
                             if (oface[o]) fix_ghosts2<R>(x, oid[o], oN[o]);
                             float2 uu, ww, mr, d1r;
-                            if constexpr (R == 2) {
-                                const float2 dm = d2p(x[0], x[1], x[2]), dc = d2p(x[1], x[2], x[3]), dp = d2p(x[2], x[3], x[4]);
-                                uu = fma2(f2s(0.5f), pick2(dm, dc), sub2(x[2], x[1]));
-                                mr = pick2(dc, dp);
-                                d1r = sub2(x[3], x[2]);
-                                ww = fma2(f2s(-0.5f), mr, d1r);
-                            } else {
-                                uu = sub2(x[1], x[0]);
-                                ww = sub2(x[2], x[1]);
-                                mr = ww; d1r = ww;
-                            }
+                            classic(x, uu, ww, mr, d1r);
                             if constexpr (PASS2) {
-                                Pt a0, a1;
-                                qpair(p, a0, a1);
-                                axis_terms(f, o, a0, a1, hih[o], uu, ww, acc[p], dis[p]);
+                                terms(o, uu, ww);
                             } else {
                                 inc_val(uu, mn[o], mx[o]);
                                 inc_val(ww, mn[o], mx[o]);
@@ -662,164 +746,68 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                         } else {
                             // pass 1, interior: the node's upper edge i+1/2 (both sides)
                             if constexpr (R == 2) {
-                                const float2 dc = d2p(sv[1][p], win[0][p], sv[2][p]);
-                                const float2 dp = d2p(win[0][p], sv[2][p], sv[3][p]);
-                                inc_edge(pick2(dc, dp), sub2(sv[2][p], win[0][p]), mn[o], mx[o]);
+                                const float2 s1 = *reinterpret_cast<const float2 *>(so + 1 * SSZ);
+                                const float2 s2 = *reinterpret_cast<const float2 *>(so + 2 * SSZ);
+                                const float2 s3 = *reinterpret_cast<const float2 *>(so + 3 * SSZ);
+                                inc_edge(pick2(d2p(s1, v0, s2), d2p(v0, s2, s3)), sub2(s2, v0), mn[o], mx[o]);
                             } else {
-                                inc_val(sub2(sv[1][p], win[0][p]), mn[o], mx[o]);
+                                inc_val(sub2(*reinterpret_cast<const float2 *>(so + 1 * SSZ), v0), mn[o], mx[o]);
                             }
                         }
                     }
-                }
 
-                // ---- in-plane rows (axis n-2) from the centre tile ----
-                {
-                    float2 rv[2 * R][NP];                  // rows -R..-1, +1..+R
-#pragma unroll
-                    for (int k = -R; k <= R; ++k) {
-                        if (k == 0) continue;
-                        if (!PASS2 && R == 2 && k == -2) continue;   // pass 1: rows -1..+2 (+ -2 from ghosts on the face)
-                        lds_p<NP>(rc + k * N1, rv[k < 0 ? k + R : k + R - 1]);
-                    }
-#pragma unroll
-                    for (int p = 0; p < NP; ++p) {
+                    // ---- in-plane rows (axis n-2): ghost rows are in the slot ----
+                    {
                         float2 x[2 * R + 1];
 #pragma unroll
-                        for (int k = -R; k <= R; ++k) x[k + R] = k == 0 ? win[0][p] : rv[k < 0 ? k + R : k + R - 1][p];
-                        if constexpr (PASS2) {
-                            if (rlo || rhi) fix_ghosts2<R>(x, grow, N2);
-                            float2 uu, ww;
-                            if constexpr (R == 2) {
-                                const float2 dm = d2p(x[0], x[1], x[2]), dc = d2p(x[1], x[2], x[3]), dp = d2p(x[2], x[3], x[4]);
-                                uu = fma2(f2s(0.5f), pick2(dm, dc), sub2(x[2], x[1]));
-                                ww = fma2(f2s(-0.5f), pick2(dc, dp), sub2(x[3], x[2]));
-                            } else {
-                                uu = sub2(x[1], x[0]);
-                                ww = sub2(x[2], x[1]);
-                            }
-                            Pt a0, a1;
-                            qpair(p, a0, a1);
-                            axis_terms(f, NDIM - 2, a0, a1, hih[NDIM - 2], uu, ww, acc[p], dis[p]);
-                        } else {
-                            if constexpr (R == 2) {
-                                // upper edge r+1/2 from rows r-1..r+2 (x[1..4]); faces in registers
-                                if (rhi) {
-                                    if (grow == N2 - 2) x[4] = ghost2(x[3], x[2], 1.f);
-                                    else { x[3] = ghost2(x[2], x[1], 1.f); x[4] = ghost2(x[2], x[1], 2.f); }
-                                }
-                                if (rlo && grow == 0) x[1] = ghost2(x[2], x[3], 1.f);
-                                const float2 dc = d2p(x[1], x[2], x[3]), dp = d2p(x[2], x[3], x[4]);
-                                const float2 m = pick2(dc, dp), d1 = sub2(x[3], x[2]);
-                                if (rhi && grow == N2 - 1) inc_val(fma2(f2s(-0.5f), m, d1), mn[NDIM - 2], mx[NDIM - 2]);
-                                else inc_edge(m, d1, mn[NDIM - 2], mx[NDIM - 2]);
-                                if (rlo && grow == 0) {            // + D-_0 of the face edge -1/2
-                                    const float2 g2 = ghost2(x[2], x[3], 2.f);
-                                    const float2 dm = d2p(g2, x[1], x[2]);
-                                    inc_val(fma2(f2s(0.5f), pick2(dm, dc), sub2(x[2], x[1])), mn[NDIM - 2], mx[NDIM - 2]);
-                                }
-                            } else {
-                                if (rhi) x[2] = ghost2(x[1], x[0], 1.f);
-                                inc_val(sub2(x[2], x[1]), mn[NDIM - 2], mx[NDIM - 2]);
-                                if (rlo) {                          // D-_0 = v_0 - ghost_{-1}
-                                    x[0] = ghost2(x[1], x[2], 1.f);
-                                    inc_val(sub2(x[1], x[0]), mn[NDIM - 2], mx[NDIM - 2]);
-                                }
-                            }
-                        }
+                        for (int k = -R; k <= R; ++k) x[k + R] = k == 0 ? v0 : *reinterpret_cast<const float2 *>(rc + k * N1);
+                        float2 uu, ww, mr, d1r;
+                        classic(x, uu, ww, mr, d1r);
+                        if constexpr (PASS2) terms(NDIM - 2, uu, ww);
+                        else { inc_val(uu, mn[NDIM - 2], mx[NDIM - 2]); inc_val(ww, mn[NDIM - 2], mx[NDIM - 2]); }
                     }
-                }
 
-                // ---- in-plane columns (axis n-1): the thread's VEC nodes share interior edges ----
-                {
-                    float c[VEC + 2 * R];                  // columns qc0-R .. qc0+VEC-1+R
+                    // ---- in-plane columns (axis n-1): left / right pairs (tile or ghost table) ----
                     {
-                        const float2 lp = *reinterpret_cast<const float2 *>(a.per1 ? rc + loff : rc - 2);
-                        const float2 rp = *reinterpret_cast<const float2 *>(a.per1 ? rc + roff : rc + VEC);
-                        if constexpr (R == 2) { c[0] = lp.x; c[1] = lp.y; } else { c[0] = lp.y; }
-#pragma unroll
-                        for (int p = 0; p < NP; ++p) { c[R + 2 * p] = win[0][p].x; c[R + 2 * p + 1] = win[0][p].y; }
-                        c[R + VEC] = rp.x;
-                        if constexpr (R == 2) c[R + VEC + 1] = rp.y;
-                    }
-                    if (clo) {
-#pragma unroll
-                        for (int k = 1; k <= R; ++k) c[R - k] = ghost(c[R], c[R + 1], (float)k);
-                    }
-                    if (chi) {
-#pragma unroll
-                        for (int k = 1; k <= R; ++k) c[R + VEC - 1 + k] = ghost(c[R + VEC - 1], c[R + VEC - 2], (float)k);
-                    }
-                    // edges e = 0 .. VEC (edge e lies between local columns e-1 and e)
-                    float em[VEC + 1], e1[VEC + 1];
-                    if constexpr (R == 2) {
-                        float d2[VEC + 2];                 // d2 at local columns -1 .. VEC
-#pragma unroll
-                        for (int k = 0; k < VEC + 2; ++k) d2[k] = d2s(c[k], c[k + 1], c[k + 2]);
-#pragma unroll
-                        for (int e = 0; e <= VEC; ++e) { em[e] = pick1(d2[e], d2[e + 1]); e1[e] = c[e + 2] - c[e + 1]; }
-                    } else {
-#pragma unroll
-                        for (int e = 0; e <= VEC; ++e) { em[e] = 0.f; e1[e] = c[e + 1] - c[e]; }
-                    }
-                    if constexpr (PASS2) {
-#pragma unroll
-                        for (int p = 0; p < NP; ++p) {
-                            const int i0 = 2 * p, i1 = 2 * p + 1;   // node i: edges i (left) and i+1 (right)
-                            float2 uu, ww;
-                            if constexpr (R == 2) {
-                                uu = fma2(f2s(0.5f), f2(em[i0], em[i1]), f2(e1[i0], e1[i1]));
-                                ww = fma2(f2s(-0.5f), f2(em[i0 + 1], em[i1 + 1]), f2(e1[i0 + 1], e1[i1 + 1]));
-                            } else {
-                                uu = f2(e1[i0], e1[i1]);
-                                ww = f2(e1[i0 + 1], e1[i1 + 1]);
-                            }
-                            Pt a0, a1;
-                            qpair(p, a0, a1);
-                            axis_terms(f, NDIM - 1, a0, a1, hih[NDIM - 1], uu, ww, acc[p], dis[p]);
-                        }
-                    } else {
-                        float &cmn = mn[NDIM - 1], &cmx = mx[NDIM - 1];
+                        const float2 lp = *reinterpret_cast<const float2 *>(rc + loff);
+                        const float2 rp = *reinterpret_cast<const float2 *>(rc + roff);
+                        float2 uu, ww;
                         if constexpr (R == 2) {
-                            inc_s(fmaf(0.5f, em[0], e1[0]), cmn, cmx);                 // D- of the first node
-#pragma unroll
-                            for (int e = 1; e + 1 < VEC; e += 2) inc_edge(f2(em[e], em[e + 1]), f2(e1[e], e1[e + 1]), cmn, cmx);
-                            if (chi) {     // last edge: D+ of the last node only
-                                inc_edge(f2(em[VEC - 1], em[VEC - 1]), f2(e1[VEC - 1], e1[VEC - 1]), cmn, cmx);
-                                inc_s(fmaf(-0.5f, em[VEC], e1[VEC]), cmn, cmx);
-                            } else {
-                                inc_edge(f2(em[VEC - 1], em[VEC]), f2(e1[VEC - 1], e1[VEC]), cmn, cmx);
-                            }
+                            // columns -2 -1 | 0 1 | 2 3 ; second differences at -1 0 1 2 ; edges -1/2, 1/2, 3/2
+                            const float dm1 = d2s(lp.x, lp.y, v0.x), d0 = d2s(lp.y, v0.x, v0.y);
+                            const float d1 = d2s(v0.x, v0.y, rp.x), d2 = d2s(v0.y, rp.x, rp.y);
+                            const float ea = pick1(dm1, d0), eb = pick1(d0, d1), ec = pick1(d1, d2);
+                            const float fa = v0.x - lp.y, fb = v0.y - v0.x, fc = rp.x - v0.y;
+                            uu = fma2(f2s(0.5f), f2(ea, eb), f2(fa, fb));
+                            ww = fma2(f2s(-0.5f), f2(eb, ec), f2(fb, fc));
                         } else {
-#pragma unroll
-                            for (int e = 0; e < VEC; e += 2) inc_val(f2(e1[e], e1[e + 1]), cmn, cmx);
-                            inc_s(e1[VEC], cmn, cmx);
+                            uu = f2(v0.x - lp.y, v0.y - v0.x);
+                            ww = f2(v0.y - v0.x, rp.x - v0.y);
                         }
+                        if constexpr (PASS2) terms(NDIM - 1, uu, ww);
+                        else { inc_val(uu, mn[NDIM - 1], mx[NDIM - 1]); inc_val(ww, mn[NDIM - 1], mx[NDIM - 1]); }
                     }
-                }
 
-                if constexpr (PASS2) {
-                    float2 o2[NP];
-#pragma unroll
-                    for (int p = 0; p < NP; ++p) {
-                        const float2 L = add2(ham_fin2(f, acc[p]), dis[p]);
-                        float2 v = fma2(f2s(dt), L, win[0][p]);                 // W + dt L
-                        if (kind == STAGE_RK2) v = mul2(f2s(0.5f), add2(vnv[p], v));   // (Vn + V2)/2 (A10)
-                        if (brt && kind != STAGE_RK1) v = f2(fminf(v.x, ttv[p].x), fminf(v.y, ttv[p].y));
-                        o2[p] = v;
+                    if constexpr (PASS2) {
+                        const float2 L = add2(ham_fin2(f, acc), dis);
+                        float2 v = fma2(f2s(dt), L, v0);                        // W + dt L
+                        if (kind == STAGE_RK2) v = mul2(f2s(0.5f), add2(vnv, v));  // (Vn + V2)/2 (A10)
+                        if (brt && kind != STAGE_RK1) v = f2(fminf(v.x, ttv.x), fminf(v.y, ttv.y));
+                        *reinterpret_cast<float2 *>(out + gi) = v;
+                        if (jg + 1 < m1) {                    // the next step's Vn / target
+                            if (kind == STAGE_RK2) vnv = *reinterpret_cast<const float2 *>(Vn + gi + M);
+                            if (brt && kind != STAGE_RK1) ttv = __ldg(reinterpret_cast<const float2 *>(T + gi + M));
+                        }
+                    } else {
+                        mabs = max3nan(mabs, fabsf(v0.x), fabsf(v0.y));
                     }
-                    st_p<NP>(out + gi, o2);
-                } else {
 #pragma unroll
-                    for (int p = 0; p < NP; ++p) mabs = max3nan(mabs, fabsf(win[0][p].x), fabsf(win[0][p].y));
+                    for (int k = 0; k < R; ++k) win[k] = win[k + 1];
                 }
-#pragma unroll
-                for (int k = 0; k < R; ++k)
-#pragma unroll
-                    for (int p = 0; p < NP; ++p) win[k][p] = win[k + 1][p];
+                __syncwarp();
+                if ((tid & 31) == 0) mbar_arrive(&empty[it & 1]);   // this warp is done with the step's buffers
+                rs0 = rs0 + 1 == RS ? 0 : rs0 + 1;
             }
-            __syncwarp();
-            if ((tid & 31) == 0) mbar_arrive(&empty[it & 1]);   // this warp is done with the step's buffers
-            rs0 = rs0 + 1 == RS ? 0 : rs0 + 1;
         }
     }
     if constexpr (!PASS2) {
@@ -941,23 +929,36 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     a.nrb = (N2 + best - 1) / best;
     a.nthr = best * QR;
     a.RSZ = geo_rsz(R, N1, best);
+    a.RGT = geo_rgt(R, N1, best);
     a.SSZ = geo_ssz(N1, best);
     a.NSS = NSS;
     a.rmarg = geo_rmarg(R, N1);
     a.side_off = geo_side_off(R, N1, best);
     a.bar_off = geo_bar_off(R, N1, best, NSS);
-    a.tab_off = a.bar_off + 8;
+    a.tab_off = a.bar_off + 16;
+    for (int o = 0; o < 3; ++o) a.sn[o] = o < MA ? g.N[o] : 1;
+    a.b1 = 1;
+    if (MA == 3) {
+        int want = 6;
+        if (const char *env = getenv("ODP_MARCH_B1")) want = std::max(1, atoi(env));
+        for (int b = std::min(want, g.N[1]); b >= 1; --b)
+            if (g.N[1] % b == 0) { a.b1 = b; break; }
+    }
     const int Nm = g.N[MA];
     long long ncols = 1;
     for (int o = 0; o < MA; ++o) ncols *= g.N[o];
     const long long cols_rb = ncols * a.nrb;
+    a.ncols = (int)std::min<long long>(ncols, 1LL << 30);
     a.K = Nm;
     if (cols_rb < 148LL * 4) a.K = std::max(4, Nm / (int)std::max<long long>(1, (148 * 8) / cols_rb));
+
     if (const char *env = getenv("ODP_MARCH_K")) a.K = std::max(1, atoi(env));
     a.K = std::min(a.K, Nm);
     a.nseg = (Nm + a.K - 1) / a.K;
     if (cols_rb * a.nseg > (1LL << 31) - 1) return false;
     a.units = (int)(cols_rb * a.nseg);
+    a.dbg = 0;
+    if (const char *env = getenv("ODP_MARCH_DBG")) a.dbg = atoi(env);
     p->block = ((a.nthr + 31) / 32) * 32 + 32;      // compute warps + the producer warp
     p->smem = (size_t)geo_smem_bytes(R, N1, best, NSS);
     p->grid = 0;
