@@ -179,24 +179,39 @@ def run_reference(args):
 def run_ours(args):
     import torch
     import paper_2204_05520_b200 as odp
-    from inputs import CONFIGS, make_v0
+    from paper_2204_05520_b200 import dist as odist
+    from inputs import CONFIGS
     rank, world, local = dist_env()
-    if world > 1:
-        from paper_2204_05520_b200 import dist as odist
-        return odist.bench_main(args)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", init_method="env://", device_id=dev)
     w = CONFIGS[args.config]
-    V0h = make_v0(w)
+    g = odist.partitioned_grid(w, rank, world, local)            # axis-0 slab of this rank (world > 1)
+    i0b, n0 = g.local_extent()
+    V0h = odist.local_v0(w, rank, world)
     V0 = torch.from_numpy(V0h).to(dev)
-    g = odp.Grid(w.N, w.lo, w.hi, w.periodic_mask)
     nout = len(w.tau) - 1
-    out = torch.empty((nout,) + w.N, dtype=torch.float32, device=dev)
+    out = torch.empty((nout,) + g.local_N, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def one(timing=False):
         return odp.hj_solve(g, w.dynamics, w.params, V0, w.tau, w.accuracy, w.mode, out=out, cfl=w.cfl,
                             kernel=args.kernel, stream=stream, timing=timing)[1]
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as tdist
+            tdist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        import torch.distributed as tdist
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
 
     for _ in range(args.warmup):
         info = one()
@@ -205,6 +220,7 @@ def run_ours(args):
     kms = {"pass1": 0.0, "pass2": 0.0, "control": 0.0}
     launches = 0
     with ClockSampler(local) as clk:
+        barrier()
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(args.steps):
@@ -214,48 +230,53 @@ def run_ours(args):
             launches += g.launch_count()
         e1.record(stream)
         torch.cuda.synchronize()
+        barrier()
     clocks = clk.summary()
-    total_ms = e0.elapsed_time(e1)
-    P = w.points
+    total_ms = max_over_ranks(e0.elapsed_time(e1))
+    P = w.points                                   # whole grid: value is the whole-job aggregate
     stages = info["stages"]
     value = P * stages * args.steps / (total_ms / 1e3)
 
-    # end to end through the C-ABI host entry point: pinned host V0 -> device -> solve -> host out
+    # end to end through the C-ABI host entry point: pinned host V0 slab -> device -> solve -> host out
     V0p = torch.from_numpy(V0h).pin_memory()
-    outp = torch.empty((nout,) + w.N, dtype=torch.float32).pin_memory()
+    outp = torch.empty((nout,) + g.local_N, dtype=torch.float32).pin_memory()
     odp.hj_solve_host(g, w.dynamics, w.params, V0p, w.tau, w.accuracy, w.mode, out=outp, cfl=w.cfl,
                       kernel=args.kernel)
-    t0 = time.perf_counter()
     e2e_steps = max(1, min(args.steps, 3))
+    barrier()
+    t0 = time.perf_counter()
     for _ in range(e2e_steps):
         odp.hj_solve_host(g, w.dynamics, w.params, V0p, w.tau, w.accuracy, w.mode, out=outp, cfl=w.cfl,
                           kernel=args.kernel)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
     e2e_value = P * stages / e2e_s
 
     peak, peak_kind = measured_peaks()
     key = (w.accuracy, w.mode)
-    n_pass2 = stages * args.steps       # one pass-2 launch per stage
+    Pl = g.points                                  # this rank's points (the kernel's launch unit)
+    n_pass2 = stages * args.steps                  # one pass-2 launch per stage
     pass2_ms = kms["pass2"] / n_pass2
     pass1_ms = kms["pass1"] / n_pass2
-    achieved = PASS2_BYTES[key] * P / (pass2_ms / 1e3) / 1e9
-    stage_gbs = STAGE_BYTES[key] * P / ((pass1_ms + pass2_ms) / 1e3) / 1e9
+    achieved = PASS2_BYTES[key] * Pl / (pass2_ms / 1e3) / 1e9
+    stage_gbs = STAGE_BYTES[key] * Pl / ((pass1_ms + pass2_ms) / 1e3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and world == 1:
         try:
-            traffic = json.load(open(prof)).get(f"{w.name}:pass2")
+            traffic = json.load(open(prof)).get(f"{w.name}:pass2")     # DRAM bytes per launch (ncu --set full)
         except Exception:
             traffic = None
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": w.name, "grid": list(w.N), "points": P, "dynamics": w.dynamics,
                    "accuracy": w.accuracy, "mode": w.mode, "cfl": w.cfl, "tau": [w.tau[0], w.tau[-1]],
                    "rk_stages_per_step": stages, "time_steps_per_step": info["steps"], "kernel": args.kernel,
-                   "l2": "inputs larger than L2 (2 x 2.9 GB working arrays)" if P * 4 > 126e6 else "fits L2",
-                   "parallelism": "single GPU"},
+                   "l2": "inputs larger than L2 (2 x %.1f GB working arrays per GPU)" % (Pl * 4 / 1e9)
+                   if Pl * 4 > 126e6 else "fits L2",
+                   "parallelism": "single GPU" if world == 1 else f"axis-0 slabs x{world} (NCCL halo + allreduce)",
+                   "slab": [i0b, n0]},
         "roofline": {"bound": "hbm", "kernel": "pass2 (D+-, H, dissipation, RK stage, BRT min)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_kind": peak_kind,
@@ -263,15 +284,21 @@ def run_ours(args):
                      "stage": {"bytes_per_point": STAGE_BYTES[key], "achieved": stage_gbs,
                                "frac": stage_gbs / peak, "pass1_ms": pass1_ms}},
         "clocks": clocks,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": P * 4, "d2h_bytes_per_step": P * 4 * nout},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": Pl * 4 * world,
+                "d2h_bytes_per_step": Pl * 4 * nout * world},
         "gpu_launches": launches,
         "kernel_ms_share": {k: v / max(total_ms, 1e-9) for k, v in kms.items()},
     }
-    if not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, sample, cores, el, pts = oracle_sample(w, target_s=args.ref_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     g.close()
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.barrier()
+        tdist.destroy_process_group()
 
 
 def main():

@@ -32,7 +32,7 @@ typedef enum {
     ODP_EINVAL = 1,    /* argument validation failed (before any device work)              */
     ODP_ENUMERIC = 2,  /* NaN or max|V| > 1e10 in a stage input (reading A19)   */
     ODP_ECUDA = 3,     /* a CUDA runtime call or kernel launch failed                       */
-    ODP_ENCCL = 4,     /* reserved for the multi-GPU transport                               */
+    ODP_ENCCL = 4,     /* an NCCL call of the multi-GPU transport failed (or NCCL missing)   */
     ODP_ENOMEM = 5     /* device or host allocation failed                                   */
 } odp_status;
 
@@ -103,7 +103,8 @@ odp_status odp_grid_create(int dims, const double *lo, const double *hi, const i
 /* Frees the handle and the device working buffers it caches.  NULL is ignored. */
 void odp_grid_destroy(odp_grid *g);
 
-/* Copies dims, N[0..dims), the spacing dx[0..dims) and the point count (any out pointer may be NULL). */
+/* Copies dims, the global N[0..dims), the spacing dx[0..dims) and the point count of the handle's
+ * (local) grid -- the whole grid unless partitioned (any out pointer may be NULL). */
 odp_status odp_grid_info(const odp_grid *g, int *dims, int64_t *N, double *dx, int64_t *points);
 
 /*
@@ -134,6 +135,32 @@ odp_status odp_hj_solve(odp_grid *g, int dynamics_id, const double *params, int 
 odp_status odp_hj_solve_host(odp_grid *g, int dynamics_id, const double *params, int nparams,
                              const float *V0, const double *tau, int ntau, int accuracy, int mode,
                              float *out, const odp_solve_opts *opts);
+
+/*
+ * Multi-GPU: axis-0 slab partition (north_star: "Large grids are slab-partitioned along axis 0 ...
+ * Each RK stage does an NCCL send/recv halo exchange over NVLink, and an allreduce-max of alpha per
+ * step"; the method's per-node independence within a stage, §4.2).
+ *
+ * odp_partition_extent -- the slab of `rank` among `nranks` over N0 axis-0 planes: contiguous,
+ *   balanced (the first N0 mod nranks ranks own one plane more).  Pure host arithmetic.
+ * odp_comm_unique_id -- writes a 128-byte NCCL unique id (call on rank 0; the caller broadcasts
+ *   it, e.g. with torch.distributed).  NCCL is loaded on first use (libnccl.so.2); ODP_ENCCL if it
+ *   cannot be loaded.
+ * odp_grid_partition -- makes the handle describe rank `rank`'s slab and joins the NCCL
+ *   communicator (collective: every rank calls it with the same id).  `device` is the CUDA device of
+ *   this rank.  After it, odp_hj_solve / odp_hj_solve_host take V0, out and target as LOCAL slab
+ *   arrays (i0_count x prod_{d>=1} N[d] floats, row-major), odp_grid_info reports the global N and
+ *   the local point count, and every stage exchanges R halo planes with the axis-0 neighbours and
+ *   allreduces the derivative range, so all ranks take the same dt sequence and the result is
+ *   bitwise the one of the unpartitioned solve.  Errors: ODP_EINVAL (rank out of range, a periodic
+ *   axis 0, fewer than 2 planes per rank, NULL id with nranks > 1), ODP_ENCCL.  nranks = 1 restores
+ *   the whole grid (with an id: a 1-rank communicator, i.e. the multi-GPU code path on one GPU).
+ * odp_grid_local_extent -- the slab of this handle: first owned axis-0 plane and the plane count.
+ */
+odp_status odp_partition_extent(int64_t N0, int nranks, int rank, int64_t *i0_begin, int64_t *i0_count);
+odp_status odp_comm_unique_id(void *id128);
+odp_status odp_grid_partition(odp_grid *g, int rank, int nranks, const void *id128, int device);
+odp_status odp_grid_local_extent(const odp_grid *g, int64_t *i0_begin, int64_t *i0_count);
 
 /* Number of kernel launches issued by the last solve on this handle (launch accounting). */
 long long odp_last_launch_count(const odp_grid *g);

@@ -125,15 +125,21 @@ def coarsened(w: Workload, N: Sequence[int], name: Optional[str] = None, tau=Non
                    tau=tuple(tau) if tau is not None else w.tau)
 
 
-def make_v0(w: Workload, seed: Optional[int] = None, noise: float = 1e-3) -> np.ndarray:
+def make_v0(w: Workload, seed: Optional[int] = None, noise: float = 1e-3, i0=None) -> np.ndarray:
     """Initial value V0 = target signed distance on the nodes, float64 -> float32 (reading A18).
 
     seed=None gives the plain workload; an integer seed adds noise*U(-1,1) from
     numpy.random.default_rng(seed) (the seeded parity variants of SURVEY.md §8(d)).
+    i0 = (begin, count) returns only the axis-0 slab [begin, begin + count) -- bitwise the same
+    values as slicing the whole array (a multi-GPU rank builds just its own slab).
     """
     axes = [axis_nodes(n, l, h, bool(p)) for n, l, h, p in zip(w.N, w.lo, w.hi, w.periodic)]
     kind = w.target[0]
     shape = w.N
+    if i0 is not None:
+        b, c = int(i0[0]), int(i0[1])
+        axes[0] = axes[0][b:b + c]
+        shape = (c,) + tuple(w.N[1:])
     if kind in ("cylinder", "sphere"):
         _, taxes, radius = w.target
         acc = np.zeros((1,) * len(shape), dtype=np.float64)
@@ -176,7 +182,10 @@ def make_v0(w: Workload, seed: Optional[int] = None, noise: float = 1e-3) -> np.
     v = np.broadcast_to(v, shape).astype(np.float64)
     if seed is not None:
         rng = np.random.default_rng(seed)
-        v = v + noise * rng.uniform(-1.0, 1.0, size=shape)
+        nz = rng.uniform(-1.0, 1.0, size=w.N)
+        if i0 is not None:
+            nz = nz[int(i0[0]):int(i0[0]) + int(i0[1])]
+        v = v + noise * nz
     return np.ascontiguousarray(v.astype(np.float32))
 
 

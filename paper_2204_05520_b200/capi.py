@@ -22,6 +22,7 @@ DYNAMICS = {"HOLONOMIC_BALL": 0, "HOLONOMIC_BOX": 1, "DUBINS3D": 2, "CAR4D": 3, 
 
 # every symbol include/odp.h declares (checked by tests/test_capi_host.py)
 EXPORTS = ("odp_grid_create", "odp_grid_destroy", "odp_grid_info", "odp_hj_solve", "odp_hj_solve_host",
+           "odp_partition_extent", "odp_comm_unique_id", "odp_grid_partition", "odp_grid_local_extent",
            "odp_last_launch_count", "odp_last_error", "odp_version")
 
 
@@ -63,6 +64,14 @@ def _load():
         f.argtypes = [vp, ctypes.c_int, D, ctypes.c_int, vp, D, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp,
                       ctypes.POINTER(odp_solve_opts)]
         f.restype = ctypes.c_int
+    lib.odp_partition_extent.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, I64, I64]
+    lib.odp_partition_extent.restype = ctypes.c_int
+    lib.odp_comm_unique_id.argtypes = [vp]
+    lib.odp_comm_unique_id.restype = ctypes.c_int
+    lib.odp_grid_partition.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int]
+    lib.odp_grid_partition.restype = ctypes.c_int
+    lib.odp_grid_local_extent.argtypes = [vp, I64, I64]
+    lib.odp_grid_local_extent.restype = ctypes.c_int
     lib.odp_last_launch_count.argtypes = [vp]
     lib.odp_last_launch_count.restype = ctypes.c_longlong
     lib.odp_last_error.argtypes = []
@@ -97,6 +106,20 @@ def _dp(a):
     return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
 
 
+def partition_extent(N0: int, nranks: int, rank: int):
+    """odp_partition_extent: (first axis-0 plane, plane count) of `rank`'s slab."""
+    b, c = ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib.odp_partition_extent(int(N0), int(nranks), int(rank), ctypes.byref(b), ctypes.byref(c)))
+    return b.value, c.value
+
+
+def comm_unique_id() -> bytes:
+    """odp_comm_unique_id: a 128-byte NCCL unique id (rank 0; broadcast it to the other ranks)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.odp_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return buf.raw
+
+
 class Grid:
     """odp_grid_create / odp_grid_destroy (P:237)."""
 
@@ -109,10 +132,11 @@ class Grid:
         _check(_lib.odp_grid_create(len(self.N), lop, hip, Na.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                                     ctypes.c_uint32(periodic_mask), ctypes.byref(h)))
         self.handle = h
+        self.local_N = self.N
 
     @property
     def points(self) -> int:
-        return int(np.prod(self.N, dtype=np.int64))
+        return int(np.prod(self.local_N, dtype=np.int64))
 
     def info(self):
         dims = ctypes.c_int()
@@ -123,6 +147,19 @@ class Grid:
                                   dx.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(P)))
         n = dims.value
         return dict(dims=n, N=tuple(N[:n]), dx=tuple(dx[:n]), points=P.value)
+
+    def partition(self, rank: int, nranks: int, uid: Optional[bytes], device: int):
+        """odp_grid_partition: this handle becomes rank `rank`'s axis-0 slab (collective over ranks)."""
+        buf = ctypes.create_string_buffer(uid, 128) if uid is not None else None
+        _check(_lib.odp_grid_partition(self.handle, int(rank), int(nranks),
+                                       ctypes.cast(buf, ctypes.c_void_p) if buf is not None else None, int(device)))
+        b, c = self.local_extent()
+        self.local_N = (c,) + self.N[1:]
+
+    def local_extent(self):
+        b, c = ctypes.c_int64(), ctypes.c_int64()
+        _check(_lib.odp_grid_local_extent(self.handle, ctypes.byref(b), ctypes.byref(c)))
+        return b.value, c.value
 
     def launch_count(self) -> int:
         return int(_lib.odp_last_launch_count(self.handle))
@@ -179,7 +216,7 @@ def hj_solve(grid: Grid, dynamics: str, params, V0, tau, accuracy: str, mode: st
     ntau = len(tau)
     nout = ntau if write_initial else ntau - 1
     if out is None:
-        out = torch.empty((nout,) + tuple(grid.N), dtype=torch.float32, device=V0.device)
+        out = torch.empty((nout,) + tuple(grid.local_N), dtype=torch.float32, device=V0.device)
     assert out.is_cuda and out.dtype == torch.float32 and out.is_contiguous() and out.numel() == nout * grid.points
     if target is not None:
         assert target.is_cuda and target.dtype == torch.float32 and target.is_contiguous()
@@ -208,7 +245,7 @@ def hj_solve_host(grid: Grid, dynamics: str, params, V0: np.ndarray, tau, accura
     ntau = len(tau)
     nout = ntau if write_initial else ntau - 1
     if out is None:
-        out = np.empty((nout,) + tuple(grid.N), dtype=np.float32)
+        out = np.empty((nout,) + tuple(grid.local_N), dtype=np.float32)
     pa, pp = _dp(params)
     ta, tp = _dp(tau)
     o, keep = _opts(cfl, host_ptr(target) if target is not None else None,

@@ -6,6 +6,7 @@
 //   -> advance] launched back to back; every kernel early-exits once the device state says the
 //   interval is done, so the host polls the 80-byte state only between chunks.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -44,19 +45,69 @@ static odp_status fail(odp_status s, const char *fmt, ...) {
     } while (0)
 
 // ------------------------------------------------------------------------------------------------
+// NCCL, loaded on first use (dlopen of libnccl.so.2: the copy torch.distributed already mapped, else
+// the system one), so single-GPU use of the library has no NCCL dependency
+// ------------------------------------------------------------------------------------------------
+namespace nccl {
+typedef int result_t;
+typedef void *comm_t;
+struct UniqueId { char internal[128]; };
+enum { Float32 = 7 };
+enum { Max = 2 };
+struct Api {
+    bool ok = false;
+    result_t (*GetUniqueId)(UniqueId *) = nullptr;
+    result_t (*CommInitRank)(comm_t *, int, UniqueId, int) = nullptr;
+    result_t (*CommDestroy)(comm_t) = nullptr;
+    result_t (*Send)(const void *, size_t, int, int, comm_t, cudaStream_t) = nullptr;
+    result_t (*Recv)(void *, size_t, int, int, comm_t, cudaStream_t) = nullptr;
+    result_t (*AllReduce)(const void *, void *, size_t, int, int, comm_t, cudaStream_t) = nullptr;
+    result_t (*GroupStart)() = nullptr;
+    result_t (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(result_t) = nullptr;
+};
+static Api &api() {
+    static Api a;
+    static bool tried = false;
+    if (tried) return a;
+    tried = true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.GetUniqueId = (result_t(*)(UniqueId *))dlsym(h, "ncclGetUniqueId");
+    a.CommInitRank = (result_t(*)(comm_t *, int, UniqueId, int))dlsym(h, "ncclCommInitRank");
+    a.CommDestroy = (result_t(*)(comm_t))dlsym(h, "ncclCommDestroy");
+    a.Send = (result_t(*)(const void *, size_t, int, int, comm_t, cudaStream_t))dlsym(h, "ncclSend");
+    a.Recv = (result_t(*)(void *, size_t, int, int, comm_t, cudaStream_t))dlsym(h, "ncclRecv");
+    a.AllReduce = (result_t(*)(const void *, void *, size_t, int, int, comm_t, cudaStream_t))dlsym(h, "ncclAllReduce");
+    a.GroupStart = (result_t(*)())dlsym(h, "ncclGroupStart");
+    a.GroupEnd = (result_t(*)())dlsym(h, "ncclGroupEnd");
+    a.GetErrorString = (const char *(*)(result_t))dlsym(h, "ncclGetErrorString");
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.AllReduce && a.GroupStart &&
+           a.GroupEnd && a.GetErrorString;
+    return a;
+}
+}  // namespace nccl
+
+#define NCCL_TRY(expr)                                                                            \
+    do {                                                                                          \
+        nccl::result_t r_ = (expr);                                                               \
+        if (r_ != 0)                                                                              \
+            return fail(ODP_ENCCL, "%s: %s (%s:%d)", #expr, nccl::api().GetErrorString(r_), __FILE__, __LINE__); \
+    } while (0)
+
+// ------------------------------------------------------------------------------------------------
 // finalize / time-loop control kernels (Alg. 2 l.164-167; readings A7, A9, A19, A20)
 // ------------------------------------------------------------------------------------------------
-template <class F, int NDIM>
-__global__ void __launch_bounds__(256) k_finalize(const float *__restrict__ partials, int nparts, DevState *st,
-                                                  GridDev g, FParams fp, const double *__restrict__ dxd,
-                                                  int stage_in_step, int final_check) {
+// Per-CTA partials of pass 1 -> one range record [-minD(n), maxD(n), maxabs, nan] (every entry a
+// max, so ranks combine records with a single allreduce(max); exact in any order).
+template <int NDIM>
+__global__ void __launch_bounds__(256) k_reduce_partials(const float *__restrict__ partials, int nparts,
+                                                         const DevState *st, float *range) {
     if (!st->active) return;
     constexpr int Q = 2 * NDIM + 2;
     __shared__ float red[Q][8];
-    __shared__ float rng[Q];
-    __shared__ int bad;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // reduce the per-CTA partials of pass 1 (min/max are exact: any order gives the same bits)
     for (int q = 0; q < Q; ++q) {
         float r = q < NDIM ? __int_as_float(0x7f800000) : (q < 2 * NDIM ? -__int_as_float(0x7f800000) : 0.f);
         for (int p = threadIdx.x; p < nparts; p += blockDim.x) {
@@ -72,6 +123,42 @@ __global__ void __launch_bounds__(256) k_finalize(const float *__restrict__ part
     }
     __syncthreads();
     if (threadIdx.x < Q) {
+        const int q = threadIdx.x;
+        float r = red[q][0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = q < NDIM ? fminf(r, red[q][w]) : fmaxf(r, red[q][w]);
+        range[q] = q < NDIM ? -r : r;
+    }
+}
+
+template <class F, int NDIM>
+__global__ void __launch_bounds__(256) k_finalize(const float *__restrict__ partials, int nparts, DevState *st,
+                                                  GridDev g, FParams fp, const double *__restrict__ dxd,
+                                                  int stage_in_step, int final_check, const float *__restrict__ range) {
+    if (!st->active) return;
+    constexpr int Q = 2 * NDIM + 2;
+    __shared__ float red[Q][8];
+    __shared__ float rng[Q];
+    __shared__ int bad;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (range) {            // multi-GPU: the range record was allreduced over the ranks
+        if (threadIdx.x < Q) rng[threadIdx.x] = threadIdx.x < NDIM ? -range[threadIdx.x] : range[threadIdx.x];
+    } else
+    // reduce the per-CTA partials of pass 1 (min/max are exact: any order gives the same bits)
+    for (int q = 0; q < Q; ++q) {
+        float r = q < NDIM ? __int_as_float(0x7f800000) : (q < 2 * NDIM ? -__int_as_float(0x7f800000) : 0.f);
+        for (int p = threadIdx.x; p < nparts; p += blockDim.x) {
+            const float o = partials[(long long)p * Q + q];
+            r = q < NDIM ? fminf(r, o) : fmaxf(r, o);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const float o = __shfl_xor_sync(0xffffffffu, r, off);
+            r = q < NDIM ? fminf(r, o) : fmaxf(r, o);
+        }
+        if (lane == 0) red[q][warp] = r;
+    }
+    __syncthreads();
+    if (!range && threadIdx.x < Q) {
         const int q = threadIdx.x;
         float r = red[q][0];
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = q < NDIM ? fminf(r, red[q][w]) : fmaxf(r, red[q][w]);
@@ -155,12 +242,14 @@ __global__ void k_advance(DevState *st) {                               // O8: t
 typedef void (*pass1_fn)(GridDev, const float *, float *, const DevState *);
 typedef void (*pass2_fn)(GridDev, const float *, const float *, const float *, float *, const DevState *, FParams,
                          int, int);
-typedef void (*fin_fn)(const float *, int, DevState *, GridDev, FParams, const double *, int, int);
+typedef void (*fin_fn)(const float *, int, DevState *, GridDev, FParams, const double *, int, int, const float *);
+typedef void (*red_fn)(const float *, int, const DevState *, float *);
 
 struct KernelSet {
     pass1_fn pass1 = nullptr;
     pass2_fn pass2 = nullptr;
     fin_fn fin = nullptr;
+    red_fn red = nullptr;
     TiledFns tiled;      // tiled family (may be empty)
     StreamFnsAll stream; // stream family (may be empty)
     MarchFnsAll march;   // march family (may be empty)
@@ -172,6 +261,7 @@ static KernelSet make_set() {
     k.pass1 = k_pass1_generic<NDIM, R>;
     k.pass2 = k_pass2_generic<F, NDIM, R>;
     k.fin = k_finalize<F, NDIM>;
+    k.red = k_reduce_partials<NDIM>;
     k.tiled = tiled_fns<F, NDIM, R>();
     k.stream = stream_fns<F, NDIM, R>();
     k.march = march_fns<F, NDIM, R>();
@@ -212,7 +302,12 @@ struct odp_grid {
     int64_t N[MAXD] = {0};
     double lo[MAXD] = {0}, hi[MAXD] = {0}, dx[MAXD] = {0};
     int per[MAXD] = {0};
-    int64_t P = 0;
+    int64_t P = 0;                // points of the whole grid
+    // axis-0 slab partition (odp_grid_partition); unpartitioned: rank 0 of 1 owning [0, N[0])
+    int rank = 0, nranks = 1;
+    int64_t i0b = 0, n0 = 0;      // first owned axis-0 plane, owned planes
+    nccl::comm_t comm = nullptr;
+    float *d_range = nullptr;     // [-minD, maxD, maxabs, nan] of the current stage (allreduced)
     // device cache (allocated lazily on the device current at the first solve)
     int device = -1;
     float *d_tab = nullptr;
@@ -239,13 +334,14 @@ static void free_device(odp_grid *g) {
     cudaSetDevice(g->device);
     cudaFree(g->d_tab); cudaFree(g->d_dx);
     cudaFree(g->d_buf[0]); cudaFree(g->d_buf[1]);
-    cudaFree(g->d_partials); cudaFree(g->d_state);
+    cudaFree(g->d_partials); cudaFree(g->d_state); cudaFree(g->d_range);
     if (g->h_state) cudaFreeHost(g->h_state);
     if (g->own_stream) cudaStreamDestroy(g->own_stream);
     for (auto e : g->events) cudaEventDestroy(e);
     g->events.clear();
     g->d_tab = nullptr; g->d_dx = nullptr; g->d_buf[0] = g->d_buf[1] = nullptr; g->d_partials = nullptr;
-    g->d_state = nullptr; g->h_state = nullptr; g->own_stream = nullptr;
+    g->d_state = nullptr; g->h_state = nullptr; g->own_stream = nullptr; g->d_range = nullptr;
+    g->max_parts = 0; g->buf_elems = 0;
     g->device = -1;
     if (cur >= 0) cudaSetDevice(cur);
 }
@@ -271,6 +367,8 @@ extern "C" odp_status odp_grid_create(int dims, const double *lo, const double *
         g->P *= N[d];
     }
     if (dims > 1 && g->P / g->N[0] > ((int64_t)1 << 31) - 1) { delete g; return fail(ODP_EINVAL, "axis-0 plane exceeds 2^31 points"); }
+    g->i0b = 0;
+    g->n0 = g->N[0];
     *out = g;
     return ODP_OK;
 }
@@ -278,7 +376,70 @@ extern "C" odp_status odp_grid_create(int dims, const double *lo, const double *
 extern "C" void odp_grid_destroy(odp_grid *g) {
     if (!g) return;
     free_device(g);
+    if (g->comm && nccl::api().ok) nccl::api().CommDestroy(g->comm);
     delete g;
+}
+
+static int64_t plane_of(const odp_grid *g) { return g->P / g->N[0]; }
+static int64_t local_points(const odp_grid *g) { return g->n0 * plane_of(g); }
+
+// Balanced contiguous axis-0 slabs: rank r owns [b, b + c) with c = floor(N0 / P) or + 1 (the first
+// N0 mod P ranks take one more plane).
+extern "C" odp_status odp_partition_extent(int64_t N0, int nranks, int rank, int64_t *i0_begin, int64_t *i0_count) {
+    g_err.clear();
+    if (nranks < 1 || rank < 0 || rank >= nranks || N0 < 1) return fail(ODP_EINVAL, "bad partition request");
+    const int64_t q = N0 / nranks, r = N0 % nranks;
+    const int64_t c = q + (rank < r ? 1 : 0);
+    const int64_t b = rank * q + (rank < r ? rank : r);
+    if (i0_begin) *i0_begin = b;
+    if (i0_count) *i0_count = c;
+    return ODP_OK;
+}
+
+extern "C" odp_status odp_comm_unique_id(void *id128) {
+    g_err.clear();
+    if (!id128) return fail(ODP_EINVAL, "NULL id");
+    nccl::Api &a = nccl::api();
+    if (!a.ok) return fail(ODP_ENCCL, "libnccl.so.2 not loadable: %s", dlerror());
+    nccl::UniqueId id;
+    NCCL_TRY(a.GetUniqueId(&id));
+    memcpy(id128, &id, sizeof id);
+    return ODP_OK;
+}
+
+// Axis-0 slab partition (north_star: slabs along axis 0, NCCL halo exchange + allreduce per stage).
+extern "C" odp_status odp_grid_partition(odp_grid *g, int rank, int nranks, const void *id128, int device) {
+    g_err.clear();
+    if (!g) return fail(ODP_EINVAL, "NULL grid");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(ODP_EINVAL, "rank %d of %d", rank, nranks);
+    if (nranks > 1 && g->per[0]) return fail(ODP_EINVAL, "axis 0 is periodic: slab partition not supported");
+    if (nranks > 1 && g->N[0] < (int64_t)R_MAX * nranks)
+        return fail(ODP_EINVAL, "N[0]=%lld < %d planes per rank", (long long)g->N[0], R_MAX);
+    if (nranks > 1 && !id128) return fail(ODP_EINVAL, "NULL NCCL id");
+    int64_t b = 0, c = 0;
+    odp_status st = odp_partition_extent(g->N[0], nranks, rank, &b, &c);
+    if (st) return st;
+    free_device(g);                       // working buffers are sized by the slab
+    if (g->comm && nccl::api().ok) nccl::api().CommDestroy(g->comm);
+    g->comm = nullptr;
+    g->rank = rank; g->nranks = nranks; g->i0b = b; g->n0 = c;
+    if (id128) {            // (nranks = 1 with an id: a 1-rank communicator -- the multi-GPU code path)
+        nccl::Api &a = nccl::api();
+        if (!a.ok) return fail(ODP_ENCCL, "libnccl.so.2 not loadable");
+        CUDA_TRY(cudaSetDevice(device));
+        nccl::UniqueId id;
+        memcpy(&id, id128, sizeof id);
+        NCCL_TRY(a.CommInitRank(&g->comm, nranks, id, rank));
+    }
+    return ODP_OK;
+}
+
+extern "C" odp_status odp_grid_local_extent(const odp_grid *g, int64_t *i0_begin, int64_t *i0_count) {
+    g_err.clear();
+    if (!g) return fail(ODP_EINVAL, "NULL grid");
+    if (i0_begin) *i0_begin = g->i0b;
+    if (i0_count) *i0_count = g->n0;
+    return ODP_OK;
 }
 
 extern "C" odp_status odp_grid_info(const odp_grid *g, int *dims, int64_t *N, double *dx, int64_t *points) {
@@ -289,7 +450,7 @@ extern "C" odp_status odp_grid_info(const odp_grid *g, int *dims, int64_t *N, do
         if (N) N[d] = g->N[d];
         if (dx) dx[d] = g->dx[d];
     }
-    if (points) *points = g->P;
+    if (points) *points = local_points(g);
     return ODP_OK;
 }
 
@@ -301,7 +462,7 @@ static odp_status ensure_device(odp_grid *g, int nparts_needed) {
     int dev = 0;
     CUDA_TRY(cudaGetDevice(&dev));
     if (g->device >= 0 && g->device != dev) free_device(g);
-    const int64_t plane = g->P / g->N[0];
+    const int64_t plane = plane_of(g);
     if (g->device < 0) {
         g->device = dev;
         // coordinate tables x, cos x, sin x per axis: float64 host values rounded to float32 (A26)
@@ -324,7 +485,7 @@ static odp_status ensure_device(odp_grid *g, int nparts_needed) {
     }
     if (!g->d_buf[0]) {
         g->halo_elems = R_MAX * plane;
-        g->buf_elems = (size_t)(g->P + 2 * g->halo_elems);
+        g->buf_elems = (size_t)(local_points(g) + 2 * g->halo_elems);
         for (int b = 0; b < 2; ++b) {
             CUDA_TRY(cudaMalloc(&g->d_buf[b], g->buf_elems * sizeof(float)));
             CUDA_TRY(cudaMemset(g->d_buf[b], 0, g->buf_elems * sizeof(float)));
@@ -336,6 +497,7 @@ static odp_status ensure_device(odp_grid *g, int nparts_needed) {
         CUDA_TRY(cudaMalloc(&g->d_partials, (size_t)nparts_needed * (2 * MAXD + 2) * sizeof(float)));
         g->max_parts = nparts_needed;
     }
+    if (!g->d_range) CUDA_TRY(cudaMalloc(&g->d_range, (2 * MAXD + 2) * sizeof(float)));
     return ODP_OK;
 }
 
@@ -354,11 +516,39 @@ static GridDev make_griddev(const odp_grid *g) {
     }
     d.stride[g->n - 1] = 1;
     for (int k = g->n - 2; k >= 0; --k) d.stride[k] = d.stride[k + 1] * g->N[k + 1];
-    d.P = g->P;
+    d.N[0] = (int)g->n0;
+    d.P = local_points(g);
     d.Ng0 = (int)g->N[0];
-    d.g0 = 0;
+    d.g0 = (int)g->i0b;
     d.tab = g->d_tab;
     return d;
+}
+
+// Halo planes of a stage input W (local plane 0) from the axis-0 neighbours (north_star: NCCL
+// send/recv per RK stage): my first R planes go to rank-1's high halo, my last R planes to rank+1's
+// low halo.  Slabs are contiguous row-major ranges, so every message is one contiguous range.
+static odp_status halo_exchange(odp_grid *g, float *W, int R, cudaStream_t s) {
+    if (g->nranks <= 1) return ODP_OK;
+    nccl::Api &a = nccl::api();
+    const size_t plane = (size_t)plane_of(g), cnt = (size_t)R * plane;
+    NCCL_TRY(a.GroupStart());
+    if (g->rank > 0) {
+        NCCL_TRY(a.Send(W, cnt, nccl::Float32, g->rank - 1, g->comm, s));
+        NCCL_TRY(a.Recv(W - cnt, cnt, nccl::Float32, g->rank - 1, g->comm, s));
+    }
+    if (g->rank < g->nranks - 1) {
+        NCCL_TRY(a.Send(W + (size_t)(g->n0 - R) * plane, cnt, nccl::Float32, g->rank + 1, g->comm, s));
+        NCCL_TRY(a.Recv(W + (size_t)g->n0 * plane, cnt, nccl::Float32, g->rank + 1, g->comm, s));
+    }
+    NCCL_TRY(a.GroupEnd());
+    return ODP_OK;
+}
+
+// allreduce(max) of the stage's range record [-minD, maxD, maxabs, nan] over the ranks
+static odp_status range_allreduce(odp_grid *g, int n, cudaStream_t s) {
+    if (!g->comm) return ODP_OK;
+    NCCL_TRY(nccl::api().AllReduce(g->d_range, g->d_range, (size_t)(2 * n + 2), nccl::Float32, nccl::Max, g->comm, s));
+    return ODP_OK;
 }
 
 static const int kWantParams[6] = {2, 3, 3, 5, 3, 3};
@@ -410,7 +600,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
         CUDA_TRY(cudaGetDevice(&dev));
         CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     }
-    long long want_blocks = (g->P + block - 1) / block;
+    long long want_blocks = (local_points(g) + block - 1) / block;
     int grid_generic = (int)std::min<long long>(want_blocks, (long long)nsm * 8);
 
     if ((st = ensure_device(g, std::max(grid_generic, nsm * 8)))) return st;
@@ -460,7 +650,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
     for (int k = 0; k < nparams; ++k) fp.c[k] = (float)params[k];
 
     float *buf[2] = {g->d_buf[0] + g->halo_elems, g->d_buf[1] + g->halo_elems};
-    const size_t bytes = (size_t)g->P * sizeof(float);
+    const size_t bytes = (size_t)local_points(g) * sizeof(float);
     g->launches = 0;
 
     CUDA_TRY(cudaMemcpyAsync(buf[0], V0, bytes, cudaMemcpyDeviceToDevice, s));
@@ -495,8 +685,20 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
         else if (use_tiled) tiled_pass2(ks.tiled, tp, gd, W, Vn, T, o, g->d_state, fp, kind, brt, s);
         else ks.pass2<<<grid_generic, block, 0, s>>>(gd, W, Vn, T, o, g->d_state, fp, kind, brt);
     };
+    odp_status cst = ODP_OK;     // first communication failure (NCCL calls are enqueued, not checked per launch)
+    auto exch = [&](float *Wx) {
+        if (g->nranks > 1 && cst == ODP_OK) cst = halo_exchange(g, Wx, R, s);
+    };
     auto launch_fin = [&](int stage_in_step, int final_check) {
-        ks.fin<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, gd, fp, g->d_dx, stage_in_step, final_check);
+        if (g->comm) {
+            ks.red<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, g->d_range);
+            if (cst == ODP_OK) cst = range_allreduce(g, n, s);
+            ks.fin<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, gd, fp, g->d_dx, stage_in_step, final_check,
+                                     g->d_range);
+        } else {
+            ks.fin<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, gd, fp, g->d_dx, stage_in_step, final_check,
+                                     nullptr);
+        }
     };
 
     // one timed/untimed launch wrapper; events are recorded only when kernel times are requested
@@ -534,13 +736,16 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
             for (int j = 0; j < chunk; ++j) {
                 const int a = (cur + j) & 1, b = a ^ 1;
                 if (accuracy == ODP_LOW) {
+                    if (g->nranks > 1 && (rs = rec(2, [&] { exch(buf[a]); }))) return rs;
                     if ((rs = rec(0, [&] { launch_pass1(buf[a]); }))) return rs;
                     if ((rs = rec(2, [&] { launch_fin(0, 0); }))) return rs;
                     if ((rs = rec(1, [&] { launch_pass2(buf[a], nullptr, buf[b], STAGE_EULER); }))) return rs;
                 } else {
+                    if (g->nranks > 1 && (rs = rec(2, [&] { exch(buf[0]); }))) return rs;
                     if ((rs = rec(0, [&] { launch_pass1(buf[0]); }))) return rs;
                     if ((rs = rec(2, [&] { launch_fin(0, 0); }))) return rs;
                     if ((rs = rec(1, [&] { launch_pass2(buf[0], nullptr, buf[1], STAGE_RK1); }))) return rs;
+                    if (g->nranks > 1 && (rs = rec(2, [&] { exch(buf[1]); }))) return rs;
                     if ((rs = rec(0, [&] { launch_pass1(buf[1]); }))) return rs;
                     if ((rs = rec(2, [&] { launch_fin(1, 0); }))) return rs;
                     if ((rs = rec(1, [&] { launch_pass2(buf[1], buf[0], buf[0], STAGE_RK2); }))) return rs;
@@ -549,6 +754,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
                 while (step_of_launch.size() < launches.size()) step_of_launch.push_back(j);
             }
             CUDA_TRY(cudaGetLastError());
+            if (cst) return cst;
             CUDA_TRY(cudaMemcpyAsync(g->h_state, g->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
             const long long done = g->h_state->steps - s0;
@@ -569,7 +775,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
             chunk = (int)std::max<long long>(1, std::min<long long>(est, 256));
         }
         if (rs != ODP_OK) break;
-        CUDA_TRY(cudaMemcpyAsync(out + (size_t)k_out * g->P, buf[accuracy == ODP_LOW ? cur : 0], bytes,
+        CUDA_TRY(cudaMemcpyAsync(out + (size_t)k_out * local_points(g), buf[accuracy == ODP_LOW ? cur : 0], bytes,
                                  cudaMemcpyDeviceToDevice, s));
         ++k_out;
     }
@@ -577,8 +783,10 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
         // final guard on the last V (reading A19)
         const float *Wf = buf[accuracy == ODP_LOW ? cur : 0];
         k_force_active<<<1, 1, 0, s>>>(g->d_state);
+        exch(const_cast<float *>(Wf));
         launch_pass1(Wf);
         launch_fin(0, 1);
+        if (cst) return cst;
         g->launches += 3;
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaMemcpyAsync(g->h_state, g->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s));
@@ -612,7 +820,7 @@ extern "C" odp_status odp_hj_solve_host(odp_grid *g, int dynamics_id, const doub
     if (!V0 || !out) return fail(ODP_EINVAL, "NULL V0/out");
     if ((st = ensure_device(g, 1))) return st;
     const int nout = (opts && opts->write_initial) ? ntau : ntau - 1;
-    const size_t bytes = (size_t)g->P * sizeof(float);
+    const size_t bytes = (size_t)local_points(g) * sizeof(float);
     cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
     float *dV0 = nullptr, *dout = nullptr, *dT = nullptr;
     CUDA_TRY(cudaMallocAsync(&dV0, bytes, s));

@@ -1,0 +1,31 @@
+"""The multi-GPU code path on one GPU: odp_grid_partition with a 1-rank NCCL communicator runs the
+stage reduction as per-CTA partials -> range record -> ncclAllReduce(max) -> finalize (the path
+every rank takes at 2/4/8 GPUs); the result must be bitwise the unpartitioned solve.  The halo
+exchange itself needs >= 2 GPUs (a single gpurun box has one)."""
+import numpy as np
+import pytest
+
+from inputs import CONFIGS, coarsened, make_v0
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name,N,acc", [("c4", (12, 10, 12, 10, 12, 10), "medium"), ("c4", (12, 10, 12, 10, 12, 10), "low"),
+                                        ("c1", (41, 41, 36), "low"), ("c3", (10, 9, 12, 9, 8), "medium")])
+@pytest.mark.parametrize("kernel", ["auto", "generic"])
+def test_one_rank_communicator_path_is_bitwise(name, N, acc, kernel):
+    import torch
+    import paper_2204_05520_b200 as odp
+    from paper_2204_05520_b200 import dist as odist
+    w = coarsened(CONFIGS[name], N, tau=(0.0, 0.05, 0.1))
+    w = w.__class__(**{**w.__dict__, "accuracy": acc, "cfl": 0.8 if acc == "low" else 0.5})
+    V0 = make_v0(w, seed=1)
+    ref, rinfo = odp.solve_workload(w, torch.from_numpy(V0).cuda(), kernel=kernel)
+    g = odist.partitioned_grid(w, 0, 1, torch.cuda.current_device(), force_comm=True)
+    assert g.local_extent() == (0, w.N[0])
+    out, info = odp.hj_solve(g, w.dynamics, w.params, torch.from_numpy(odist.local_v0(w, 0, 1, seed=1)).cuda(),
+                             w.tau, w.accuracy, w.mode, cfl=w.cfl, kernel=kernel)
+    torch.cuda.synchronize()
+    assert info["steps"] == rinfo["steps"] and info["stages"] == rinfo["stages"]
+    np.testing.assert_array_equal(out.cpu().numpy(), ref.cpu().numpy())
+    g.close()
