@@ -49,9 +49,11 @@ if os.path.exists(rep):
     traffic = {}
     for r in rr[2:]:
         d = dict(zip(h, r))
-        kind = "pass2" if re.search(r", (true|1)>", d["Kernel Name"]) else "pass1"
-        rd_b = float(d["dram__bytes_read.sum"]) * (1e9 if rr[1][h.index("dram__bytes_read.sum")].startswith("G") else 1)
-        wr_b = float(d["dram__bytes_write.sum"]) * (1e9 if rr[1][h.index("dram__bytes_write.sum")].startswith("G") else 1)
+        targs = re.search(r"<([^>]*)>", d["Kernel Name"]).group(1).split(", ")
+        kind = "pass2" if targs[4].strip() in ("1", "true", "(bool)1") else "pass1"
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        rd_b = float(d["dram__bytes_read.sum"]) * scale[rr[1][h.index("dram__bytes_read.sum")]]
+        wr_b = float(d["dram__bytes_write.sum"]) * scale[rr[1][h.index("dram__bytes_write.sum")]]
         traffic[f"c4:{kind}"] = rd_b + wr_b
         traffic[f"c4:{kind}:kernel"] = re.sub(r"\(.*", "", d["Kernel Name"])
     traffic["_source"] = f"profiles/{tag}_ncu_full_summary.txt (dram__bytes_read.sum + dram__bytes_write.sum, one launch each)"

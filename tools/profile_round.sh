@@ -7,5 +7,5 @@ cat gpurun_out/bench.json
 python tools/profile_run.py c4 0.05 > gpurun_out/plain_prof.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python tools/profile_run.py c4 0.05 > gpurun_out/ncu_launches.log 2>&1
 tail -1 gpurun_out/ncu_launches.log
-ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-k_stream} -s 0 -c 2 -o gpurun_out/prof_full python tools/profile_run.py c4 0.02 > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-k_march} -s 0 -c 2 -o gpurun_out/prof_full python tools/profile_run.py c4 0.02 > gpurun_out/ncu_full.log 2>&1
 tail -1 gpurun_out/ncu_full.log
