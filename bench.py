@@ -289,6 +289,26 @@ def run_ours(args):
         "gpu_launches": launches,
         "kernel_ms_share": {k: v / max(total_ms, 1e-9) for k, v in kms.items()},
     }
+    if args.single_pass_too:
+        # the same solve without pass 1 after the first step (alpha^max fixed for a
+        # functor whose alpha does not depend on the derivative range); bitwise the two-pass result
+        ref = out.clone()
+        sp_info = odp.hj_solve(g, w.dynamics, w.params, V0, w.tau, w.accuracy, w.mode, out=out, cfl=w.cfl,
+                               kernel=args.kernel, stream=stream, single_pass=True)[1]
+        torch.cuda.synchronize()
+        same = bool(torch.equal(out, ref))
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            sp_info = odp.hj_solve(g, w.dynamics, w.params, V0, w.tau, w.accuracy, w.mode, out=out, cfl=w.cfl,
+                                   kernel=args.kernel, stream=stream, single_pass=True)[1]
+        e1.record(stream)
+        torch.cuda.synchronize()
+        sp_ms = max_over_ranks(e0.elapsed_time(e1))
+        line["single_pass"] = {"value": P * stages * args.steps / (sp_ms / 1e3), "unit": UNIT,
+                               "ms_per_step": sp_ms / args.steps, "used": bool(sp_info["single_pass"]),
+                               "bitwise_equal_to_two_pass": same,
+                               "note": "SURVEY.md §8(f1) variant, not the headline (Alg. 2's two passes)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, sample, cores, el, pts = oracle_sample(w, target_s=args.ref_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
@@ -310,6 +330,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "generic", "tiled", "stream", "march"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--single-pass-too", type=int, default=1,
+                    help="also time the single-pass variant (SURVEY.md §8(f1)) and report it beside the headline")
     ap.add_argument("--ref-seconds", type=float, default=15.0)
     args = ap.parse_args()
     if args.impl == "reference":

@@ -88,6 +88,13 @@ typedef struct {
     long long *steps_taken;   /* optional out: time steps taken                                     */
     long long *stages_taken;  /* optional out: RK stages evaluated                                  */
     double *kernel_ms;        /* optional out [3]: summed device time of pass 1, pass 2, finalize   */
+    int single_pass;          /* 1 -> SURVEY.md §8(f1): when the functor's alpha does not depend on
+                                 the derivative range (HOLONOMIC_BOX, DUBINS3D, CAR5D, DOUBLEINT6D)
+                                 and the march kernels cover the grid, skip pass 1 after the first
+                                 step: alpha^max is fixed, dt is re-derived from it, and the guard
+                                 (NaN, |V| > 1e10) checks every stage's output.  Bitwise the
+                                 two-pass result.  0 (default) -> Algorithm 2's two passes        */
+    int *single_pass_used;    /* optional out: 1 if the single-pass path ran                      */
 } odp_solve_opts;
 
 /*

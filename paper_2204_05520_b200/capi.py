@@ -36,7 +36,9 @@ class odp_solve_opts(ctypes.Structure):
                 ("tau_reached", ctypes.POINTER(ctypes.c_double)),
                 ("steps_taken", ctypes.POINTER(ctypes.c_longlong)),
                 ("stages_taken", ctypes.POINTER(ctypes.c_longlong)),
-                ("kernel_ms", ctypes.POINTER(ctypes.c_double))]
+                ("kernel_ms", ctypes.POINTER(ctypes.c_double)),
+                ("single_pass", ctypes.c_int),
+                ("single_pass_used", ctypes.POINTER(ctypes.c_int))]
 
 
 class OdpError(RuntimeError):
@@ -180,7 +182,7 @@ class SolveInfo(dict):
     pass
 
 
-def _opts(cfl, target_ptr, stream_ptr, write_initial, kernel, timing):
+def _opts(cfl, target_ptr, stream_ptr, write_initial, kernel, timing, single_pass=False):
     o = odp_solve_opts()
     o.cfl = float(cfl or 0.0)
     o.target = target_ptr
@@ -196,12 +198,16 @@ def _opts(cfl, target_ptr, stream_ptr, write_initial, kernel, timing):
     o.steps_taken = ctypes.pointer(st)
     o.stages_taken = ctypes.pointer(sg)
     o.kernel_ms = ctypes.cast(km, ctypes.POINTER(ctypes.c_double)) if timing else None
-    return o, (tr, st, sg, km)
+    o.single_pass = int(bool(single_pass))
+    spu = ctypes.c_int()
+    o.single_pass_used = ctypes.pointer(spu)
+    return o, (tr, st, sg, km, spu)
 
 
 def _info(keep, timing, status):
-    tr, st, sg, km = keep
-    info = SolveInfo(tau_reached=tr.value, steps=st.value, stages=sg.value, status=status)
+    tr, st, sg, km, spu = keep
+    info = SolveInfo(tau_reached=tr.value, steps=st.value, stages=sg.value, status=status,
+                     single_pass=bool(spu.value))
     if timing:
         info["kernel_ms"] = dict(pass1=km[0], pass2=km[1], control=km[2])
     return info
@@ -209,7 +215,7 @@ def _info(keep, timing, status):
 
 def hj_solve(grid: Grid, dynamics: str, params, V0, tau, accuracy: str, mode: str, out=None, cfl: float = 0.0,
              target=None, write_initial: bool = False, kernel: str = "auto", stream=None, timing: bool = False,
-             raise_on_error: bool = True):
+             raise_on_error: bool = True, single_pass: bool = False):
     """odp_hj_solve on torch CUDA tensors (device pointers).  Returns (out, info)."""
     import torch
     assert V0.is_cuda and V0.dtype == torch.float32 and V0.is_contiguous()
@@ -225,7 +231,7 @@ def hj_solve(grid: Grid, dynamics: str, params, V0, tau, accuracy: str, mode: st
     pa, pp = _dp(params)
     ta, tp = _dp(tau)
     o, keep = _opts(cfl, target.data_ptr() if target is not None else None, stream.cuda_stream, write_initial,
-                    kernel, timing)
+                    kernel, timing, single_pass)
     status = _lib.odp_hj_solve(grid.handle, DYNAMICS[dynamics], pp, len(pa), V0.data_ptr(), tp, len(ta),
                                ACCURACY[accuracy], MODE[mode], out.data_ptr(), ctypes.byref(o))
     if status != ODP_OK and raise_on_error:
@@ -235,7 +241,7 @@ def hj_solve(grid: Grid, dynamics: str, params, V0, tau, accuracy: str, mode: st
 
 def hj_solve_host(grid: Grid, dynamics: str, params, V0: np.ndarray, tau, accuracy: str, mode: str, out=None,
                   cfl: float = 0.0, target=None, write_initial: bool = False, kernel: str = "auto", stream=None,
-                  timing: bool = False, raise_on_error: bool = True):
+                  timing: bool = False, raise_on_error: bool = True, single_pass: bool = False):
     """odp_hj_solve_host: V0/out/target are host arrays (numpy or pinned torch CPU tensors)."""
     def host_ptr(a):
         if hasattr(a, "data_ptr"):
@@ -249,7 +255,7 @@ def hj_solve_host(grid: Grid, dynamics: str, params, V0: np.ndarray, tau, accura
     pa, pp = _dp(params)
     ta, tp = _dp(tau)
     o, keep = _opts(cfl, host_ptr(target) if target is not None else None,
-                    stream.cuda_stream if stream is not None else None, write_initial, kernel, timing)
+                    stream.cuda_stream if stream is not None else None, write_initial, kernel, timing, single_pass)
     status = _lib.odp_hj_solve_host(grid.handle, DYNAMICS[dynamics], pp, len(pa), host_ptr(V0), tp, len(ta),
                                     ACCURACY[accuracy], MODE[mode], host_ptr(out), ctypes.byref(o))
     if status != ODP_OK and raise_on_error:

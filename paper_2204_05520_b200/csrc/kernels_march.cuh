@@ -794,6 +794,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                         if (kind == STAGE_RK2) v = mul2(f2s(0.5f), add2(vnv, v));  // (Vn + V2)/2 (A10)
                         if (brt && kind != STAGE_RK1) v = f2(fminf(v.x, ttv.x), fminf(v.y, ttv.y));
                         *reinterpret_cast<float2 *>(out + gi) = v;
+                        mabs = max3nan(mabs, fabsf(v.x), fabsf(v.y));   // output guard (single-pass solves)
                         if (jg + 1 < m1) {                    // the next step's Vn / target
                             if (kind == STAGE_RK2) vnv = *reinterpret_cast<const float2 *>(Vn + gi + M);
                             if (brt && kind != STAGE_RK1) ttv = __ldg(reinterpret_cast<const float2 *>(T + gi + M));
@@ -813,6 +814,11 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     if constexpr (!PASS2) {
 #pragma unroll
         for (int d = 0; d < NDIM; ++d) { mn[d] *= g.inv_dx[d]; mx[d] *= g.inv_dx[d]; }   // h D -> D
+        const int nan = mabs != mabs;
+        block_reduce_range<NDIM>(mn, mx, nan ? 0.f : mabs, nan, partials);
+    } else if (partials) {
+        // single-pass solves: the guard of A19 on this stage's OUTPUT -- the next
+        // stage's input -- in place of pass 1 (the range entries stay neutral)
         const int nan = mabs != mabs;
         block_reduce_range<NDIM>(mn, mx, nan ? 0.f : mabs, nan, partials);
     }
@@ -987,8 +993,8 @@ inline void march_pass1(const MarchFns &t, const MarchPlan &p, const GridDev &g,
 
 inline void march_pass2(const MarchFns &t, const MarchPlan &p, const GridDev &g, const float *W, const float *Vn,
                         const float *T, float *out, const DevState *st, const FParams &fp, int kind, int brt,
-                        cudaStream_t s) {
-    t.pass2<<<p.grid, p.block, p.smem, s>>>(p.a, g, W, Vn, T, out, nullptr, st, fp, kind, brt);
+                        cudaStream_t s, float *guard_partials = nullptr) {
+    t.pass2<<<p.grid, p.block, p.smem, s>>>(p.a, g, W, Vn, T, out, guard_partials, st, fp, kind, brt);
 }
 
 }  // namespace odp

@@ -218,16 +218,75 @@ __global__ void __launch_bounds__(256) k_finalize(const float *__restrict__ part
 
 __global__ void k_init_state(DevState *st, double cfl, double eps) {
     st->tau = 0.0; st->tau_target = 0.0; st->eps = eps; st->dt = 0.0; st->cfl = cfl; st->dt_f = 0.f;
-    st->maxabs = 0.f; st->nan = 0; st->active = 0; st->status = 0; st->steps = 0; st->stages = 0;
+    st->maxabs = 0.f; st->nan = 0; st->active = 0; st->status = 0; st->steps = 0; st->stages = 0; st->pending = 0;
     for (int d = 0; d < MAXD; ++d) { st->minD[d] = 0.f; st->maxD[d] = 0.f; st->amax[d] = 0.f; }
 }
 
 __global__ void k_begin(DevState *st, double tau_k) {
+    if (st->pending) { st->status = ODP_ENUMERIC; st->pending = 0; }
     st->tau_target = tau_k;
     st->active = (st->status == 0 && tau_k - st->tau > st->eps) ? 1 : 0;
 }
 
-__global__ void k_force_active(DevState *st) { st->active = st->status == 0 ? 1 : 0; }
+__global__ void k_force_active(DevState *st) {
+    if (st->pending) { st->status = ODP_ENUMERIC; st->pending = 0; }
+    st->active = st->status == 0 ? 1 : 0;
+}
+
+// Single-pass solves: for a functor whose alpha_(i,d) does not depend on the
+// derivative range (RANGE_FREE), alpha^max is the same at every step, so pass 1 is dead work apart
+// from the guard of A19.  k_dt re-derives dt from the stored alpha^max exactly as k_finalize does
+// (same float64 expression); k_guard checks the stage OUTPUT (= the next stage's input) from the
+// max|V| / NaN partials pass 2 wrote, and counts the stage.
+__global__ void k_dt(DevState *st, const double *__restrict__ dxd, int n) {
+    if (!st->active) return;
+    if (st->pending) { st->status = ODP_ENUMERIC; st->active = 0; return; }   // detected at this stage's input
+    double sum = 0.0;                                                 // Alg. 2 l.167
+    for (int d = 0; d < n; ++d) sum += fabs((double)st->amax[d]) / dxd[d];
+    const double rem = st->tau_target - st->tau;
+    double dt = sum > 0.0 ? st->cfl / sum : rem;                      // A20
+    if (dt > rem) dt = rem;                                           // A9
+    st->dt = dt;
+    st->dt_f = (float)dt;
+}
+
+template <int NDIM>
+__global__ void __launch_bounds__(256) k_guard(const float *__restrict__ partials, int nparts, DevState *st,
+                                               const float *__restrict__ range, int last_stage) {
+    if (!st->active) return;
+    constexpr int Q = 2 * NDIM + 2;
+    __shared__ float red[2][8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float ma = 0.f, nn = 0.f;
+    if (range) {
+        ma = range[2 * NDIM]; nn = range[2 * NDIM + 1];
+    } else {
+        for (int p = threadIdx.x; p < nparts; p += blockDim.x) {
+            ma = fmaxf(ma, partials[(long long)p * Q + 2 * NDIM]);
+            nn = fmaxf(nn, partials[(long long)p * Q + 2 * NDIM + 1]);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, off));
+            nn = fmaxf(nn, __shfl_xor_sync(0xffffffffu, nn, off));
+        }
+        if (lane == 0) { red[0][warp] = ma; red[1][warp] = nn; }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { ma = fmaxf(ma, red[0][w]); nn = fmaxf(nn, red[1][w]); }
+    }
+    if (threadIdx.x == 0) {
+        st->stages += 1;                                              // the stage ran on a checked input
+        if (nn != 0.f || !(ma <= 1e10f)) {
+            // the two-pass solve detects this at the next stage's input: within the step (RK stage 1)
+            // that stops the step; after its last stage the step completes (tau advances) first
+            st->nan = nn != 0.f;
+            if (last_stage) st->pending = 1;
+            else { st->status = ODP_ENUMERIC; st->active = 0; }
+        }
+        st->maxabs = ma;
+    }
+}
 
 __global__ void k_advance(DevState *st) {                               // O8: tau += dt (float64)
     if (!st->active) return;
@@ -244,12 +303,15 @@ typedef void (*pass2_fn)(GridDev, const float *, const float *, const float *, f
                          int, int);
 typedef void (*fin_fn)(const float *, int, DevState *, GridDev, FParams, const double *, int, int, const float *);
 typedef void (*red_fn)(const float *, int, const DevState *, float *);
+typedef void (*guard_fn)(const float *, int, DevState *, const float *, int);
 
 struct KernelSet {
     pass1_fn pass1 = nullptr;
     pass2_fn pass2 = nullptr;
     fin_fn fin = nullptr;
     red_fn red = nullptr;
+    guard_fn guard = nullptr;
+    bool range_free = false;
     TiledFns tiled;      // tiled family (may be empty)
     StreamFnsAll stream; // stream family (may be empty)
     MarchFnsAll march;   // march family (may be empty)
@@ -262,6 +324,8 @@ static KernelSet make_set() {
     k.pass2 = k_pass2_generic<F, NDIM, R>;
     k.fin = k_finalize<F, NDIM>;
     k.red = k_reduce_partials<NDIM>;
+    k.guard = k_guard<NDIM>;
+    k.range_free = F::RANGE_FREE;
     k.tiled = tiled_fns<F, NDIM, R>();
     k.stream = stream_fns<F, NDIM, R>();
     k.march = march_fns<F, NDIM, R>();
@@ -679,13 +743,25 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
         else if (use_tiled) tiled_pass1(ks.tiled, tp, gd, W, g->d_partials, g->d_state, s);
         else ks.pass1<<<grid_generic, block, 0, s>>>(gd, W, g->d_partials, g->d_state);
     };
-    auto launch_pass2 = [&](const float *W, const float *Vn, float *o, int kind) {
-        if (use_march) march_pass2(mfn, mp, gd, W, Vn, T, o, g->d_state, fp, kind, brt, s);
+    // single-pass: opted in, RANGE_FREE functor, march family
+    const bool single = opts && opts->single_pass && ks.range_free && use_march;
+    bool have_amax = false;              // alpha^max of this solve computed by a two-pass step
+    auto launch_pass2 = [&](const float *W, const float *Vn, float *o, int kind, bool guard = false) {
+        if (use_march) march_pass2(mfn, mp, gd, W, Vn, T, o, g->d_state, fp, kind, brt, s, guard ? g->d_partials : nullptr);
         else if (use_stream) stream_pass2(sfn, sp, gd, W, Vn, T, o, g->d_state, fp, kind, brt, s);
         else if (use_tiled) tiled_pass2(ks.tiled, tp, gd, W, Vn, T, o, g->d_state, fp, kind, brt, s);
         else ks.pass2<<<grid_generic, block, 0, s>>>(gd, W, Vn, T, o, g->d_state, fp, kind, brt);
     };
     odp_status cst = ODP_OK;     // first communication failure (NCCL calls are enqueued, not checked per launch)
+    auto launch_guard = [&](int last_stage) {
+        if (g->comm) {
+            ks.red<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, g->d_range);
+            if (cst == ODP_OK) cst = range_allreduce(g, n, s);
+            ks.guard<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, g->d_range, last_stage);
+        } else {
+            ks.guard<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, nullptr, last_stage);
+        }
+    };
     auto exch = [&](float *Wx) {
         if (g->nranks > 1 && cst == ODP_OK) cst = halo_exchange(g, Wx, R, s);
     };
@@ -735,7 +811,22 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
             ev_next = 0;
             for (int j = 0; j < chunk; ++j) {
                 const int a = (cur + j) & 1, b = a ^ 1;
-                if (accuracy == ODP_LOW) {
+                if (single && have_amax) {
+                    // pass 2 only: dt from the fixed alpha^max, the guard on each stage's output
+                    if ((rs = rec(2, [&] { k_dt<<<1, 1, 0, s>>>(g->d_state, g->d_dx, n); }))) return rs;
+                    if (accuracy == ODP_LOW) {
+                        if (g->nranks > 1 && (rs = rec(2, [&] { exch(buf[a]); }))) return rs;
+                        if ((rs = rec(1, [&] { launch_pass2(buf[a], nullptr, buf[b], STAGE_EULER, true); }))) return rs;
+                        if ((rs = rec(2, [&] { launch_guard(1); }))) return rs;
+                    } else {
+                        if (g->nranks > 1 && (rs = rec(2, [&] { exch(buf[0]); }))) return rs;
+                        if ((rs = rec(1, [&] { launch_pass2(buf[0], nullptr, buf[1], STAGE_RK1, true); }))) return rs;
+                        if ((rs = rec(2, [&] { launch_guard(0); }))) return rs;
+                        if (g->nranks > 1 && (rs = rec(2, [&] { exch(buf[1]); }))) return rs;
+                        if ((rs = rec(1, [&] { launch_pass2(buf[1], buf[0], buf[0], STAGE_RK2, true); }))) return rs;
+                        if ((rs = rec(2, [&] { launch_guard(1); }))) return rs;
+                    }
+                } else if (accuracy == ODP_LOW) {
                     if (g->nranks > 1 && (rs = rec(2, [&] { exch(buf[a]); }))) return rs;
                     if ((rs = rec(0, [&] { launch_pass1(buf[a]); }))) return rs;
                     if ((rs = rec(2, [&] { launch_fin(0, 0); }))) return rs;
@@ -751,6 +842,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
                     if ((rs = rec(1, [&] { launch_pass2(buf[1], buf[0], buf[0], STAGE_RK2); }))) return rs;
                 }
                 if ((rs = rec(2, [&] { k_advance<<<1, 1, 0, s>>>(g->d_state); }))) return rs;
+                have_amax = true;
                 while (step_of_launch.size() < launches.size()) step_of_launch.push_back(j);
             }
             CUDA_TRY(cudaGetLastError());
@@ -798,6 +890,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
         if (opts->steps_taken) *opts->steps_taken = g->h_state->steps;
         if (opts->stages_taken) *opts->stages_taken = g->h_state->stages;
         if (opts->kernel_ms) for (int q = 0; q < 3; ++q) opts->kernel_ms[q] = kms[q];
+        if (opts->single_pass_used) *opts->single_pass_used = single ? 1 : 0;
     }
     if (rs == ODP_ENUMERIC)
         return fail(ODP_ENUMERIC, "numerical failure (NaN or |V| > 1e10) at tau = %.9g", g->h_state->tau);

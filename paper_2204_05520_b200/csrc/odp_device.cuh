@@ -48,6 +48,7 @@ struct DevState {
     int nan;
     int active;          // 1 while the current save interval still needs steps
     int status;          // 0 ok, 2 numeric failure (A19)
+    int pending;         // single-pass: the last stage's OUTPUT failed the guard; fail at the next stage's start
     long long steps, stages;
 };
 
@@ -133,6 +134,8 @@ struct SignSet {
 
 template <int NDIM>
 struct FHoloBall {   // [ubar, goal]: xdot = u, |u|_2 <= ubar
+    // alpha_(i,d) does not depend on the stage's derivative range: false
+    static constexpr bool RANGE_FREE = false;
     static constexpr int NEED_X = 0, NEED_TRIG = 0;
     static __host__ __device__ int deps(int) { return 0; }
     float kH, a[NDIM];
@@ -162,6 +165,8 @@ struct FHoloBall {   // [ubar, goal]: xdot = u, |u|_2 <= ubar
 
 template <int NDIM>
 struct FHoloBox {    // [ubar, dbar, goal]: xdot_i = u_i + d_i
+    // alpha_(i,d) does not depend on the stage's derivative range: true
+    static constexpr bool RANGE_FREE = true;
     static constexpr int NEED_X = 0, NEED_TRIG = 0;
     static __host__ __device__ int deps(int) { return 0; }
     float kH, a[NDIM];
@@ -184,6 +189,8 @@ struct FHoloBox {    // [ubar, dbar, goal]: xdot_i = u_i + d_i
 };
 
 struct FDubins3D {   // [v, wbar, goal]: (x, y, th) -> (v cos th, v sin th, w)
+    // alpha_(i,d) does not depend on the stage's derivative range: true
+    static constexpr bool RANGE_FREE = true;
     static constexpr int NDIM = 3;
     static constexpr int NEED_X = 0, NEED_TRIG = 1 << 2;
     static __host__ __device__ int deps(int d) { return d < 2 ? (1 << 2) : 0; }
@@ -203,6 +210,8 @@ struct FDubins3D {   // [v, wbar, goal]: (x, y, th) -> (v cos th, v sin th, w)
 };
 
 struct FCar4D {      // [abar, wbar, dxbar, dybar, goal]: (x, y, v, th)
+    // alpha_(i,d) does not depend on the stage's derivative range: false
+    static constexpr bool RANGE_FREE = false;
     static constexpr int NDIM = 4;
     static constexpr int NEED_X = 1 << 2, NEED_TRIG = 1 << 3;
     static __host__ __device__ int deps(int d) { return d < 2 ? ((1 << 2) | (1 << 3)) : 0; }
@@ -234,6 +243,8 @@ struct FCar4D {      // [abar, wbar, dxbar, dybar, goal]: (x, y, v, th)
 };
 
 struct FCar5D {      // [abar, alphabar, goal]: (x, y, th, v, w)
+    // alpha_(i,d) does not depend on the stage's derivative range: true
+    static constexpr bool RANGE_FREE = true;
     static constexpr int NDIM = 5;
     static constexpr int NEED_X = (1 << 3) | (1 << 4), NEED_TRIG = 1 << 2;
     static __host__ __device__ int deps(int d) {
@@ -263,6 +274,8 @@ struct FCar5D {      // [abar, alphabar, goal]: (x, y, th, v, w)
 };
 
 struct FDoubleInt6D {  // [ubar, dbar, goal]: (px, vx, py, vy, pz, vz) -> (v_i, u_i + d_i)
+    // alpha_(i,d) does not depend on the stage's derivative range: true
+    static constexpr bool RANGE_FREE = true;
     static constexpr int NDIM = 6;
     static constexpr int NEED_X = (1 << 1) | (1 << 3) | (1 << 5), NEED_TRIG = 0;
     static __host__ __device__ int deps(int d) { return (d & 1) == 0 ? (1 << (d + 1)) : 0; }

@@ -29,3 +29,38 @@ def test_one_rank_communicator_path_is_bitwise(name, N, acc, kernel):
     assert info["steps"] == rinfo["steps"] and info["stages"] == rinfo["stages"]
     np.testing.assert_array_equal(out.cpu().numpy(), ref.cpu().numpy())
     g.close()
+
+
+@pytest.mark.parametrize("name,N,acc", [("c4", (12, 10, 12, 10, 12, 10), "medium"), ("c4", (12, 10, 12, 10, 12, 10), "low"),
+                                        ("c1", (41, 41, 36), "low"), ("c3", (10, 9, 12, 9, 8), "medium"),
+                                        ("c2", (14, 12, 12, 16), "low")])
+def test_single_pass_is_bitwise_the_two_pass_solve(name, N, acc):
+    # for functors whose alpha does not depend on the derivative range the
+    # single-pass path skips pass 1 after the first step; same alpha, same dt sequence, same arithmetic
+    import torch
+    import paper_2204_05520_b200 as odp
+    w = coarsened(CONFIGS[name], N, tau=(0.0, 0.05, 0.1))
+    w = w.__class__(**{**w.__dict__, "accuracy": acc, "cfl": 0.8 if acc == "low" else 0.5})
+    V0 = torch.from_numpy(make_v0(w, seed=2)).cuda()
+    ref, rinfo = odp.solve_workload(w, V0)
+    out, info = odp.solve_workload(w, V0, single_pass=True)
+    assert info["single_pass"] == (name != "c2")      # CAR4D's alpha depends on the range's sign set
+    assert info["steps"] == rinfo["steps"] and info["stages"] == rinfo["stages"]
+    np.testing.assert_array_equal(out.cpu().numpy(), ref.cpu().numpy())
+
+
+def test_single_pass_guard_reports_divergence():
+    import torch
+    import paper_2204_05520_b200 as odp
+    from inputs import Workload
+    import oracle
+    w = Workload("div", (21, 21, 20), (-1.0, -1.0, -1.0), (1.0, 1.0, 1.0), (0, 0, 0), "HOLONOMIC_BOX",
+                 (1.0, 0.0, -1.0), (0.0, 50.0), "low", 40.0, "brs", ("random_smooth", 3))
+    V0 = make_v0(w)
+    ref = oracle.solve_workload(w, V0=V0, raise_on_error=False)
+    out, info = odp.solve_workload(w, torch.from_numpy(V0).cuda(), raise_on_error=False, single_pass=True)
+    two, tinfo = odp.solve_workload(w, torch.from_numpy(V0).cuda(), raise_on_error=False)
+    assert ref.status == 2 and info["status"] == 2 and tinfo["status"] == 2
+    assert info["single_pass"]
+    assert info["steps"] == tinfo["steps"] == ref.steps and info["stages"] == tinfo["stages"]
+    assert info["tau_reached"] == tinfo["tau_reached"]
