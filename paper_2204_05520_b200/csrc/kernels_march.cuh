@@ -284,13 +284,14 @@ __host__ __device__ constexpr int geo_rgt(int R, int N1, int B) {
 }
 __host__ __device__ constexpr int geo_rsz(int R, int N1, int B) { return geo_rgt(R, N1, B) + 4 * (B + 2 * R); }
 __host__ __device__ constexpr int geo_ssz(int N1, int B) { return ((MARCH_SMARG + B * N1 + 3) / 4) * 4; }
-__host__ __device__ constexpr int geo_side_off(int R, int N1, int B) { return (R + 2) * geo_rsz(R, N1, B); }
-__host__ __device__ constexpr int geo_bar_off(int R, int N1, int B, int NSS) {
-    return ((geo_side_off(R, N1, B) + 2 * NSS * geo_ssz(N1, B)) + 3) / 4 * 4;
+// NST pipeline stages: NST side buffers, R + NST ring slots
+__host__ __device__ constexpr int geo_side_off(int R, int N1, int B, int NST) { return (R + NST) * geo_rsz(R, N1, B); }
+__host__ __device__ constexpr int geo_bar_off(int R, int N1, int B, int NSS, int NST) {
+    return ((geo_side_off(R, N1, B, NST) + NST * NSS * geo_ssz(N1, B)) + 3) / 4 * 4;
 }
-// 6 mbarriers (48 B, padded to 64) + copy table: 32 x 8 B offsets + 32 x 4 B sizes + 8 x 4 B ring fields
-__host__ __device__ constexpr int geo_smem_bytes(int R, int N1, int B, int NSS) {
-    return geo_bar_off(R, N1, B, NSS) * 4 + 64 + 32 * 8 + 32 * 4 + 8 * 4;
+// <= 16 mbarriers (128 B) + copy table: 32 x 8 B offsets + 32 x 4 B sizes + 8 x 4 B ring fields
+__host__ __device__ constexpr int geo_smem_bytes(int R, int N1, int B, int NSS, int NST) {
+    return geo_bar_off(R, N1, B, NSS, NST) * 4 + 128 + 32 * 8 + 32 * 4 + 8 * 4 + 16;   // + unit queue
 }
 
 struct MarchUnit {
@@ -359,17 +360,21 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) 
     }
 }
 
-template <class F, int NDIM, int R, int NP, bool PASS2, int CN1 = 0, int CB = 0>
+template <class F, int NDIM, int R, int NP, bool PASS2, int CN1 = 0, int CB = 0, int NST = 2>
 __global__ void __launch_bounds__(MARCH_MAXT1, ODP_MARCH_MINB1)
 k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, const float *__restrict__ T,
         float *out, float *partials, const DevState *st, FParams fp, int kind, int brt) {
     static_assert(NP == 1, "the march family computes node pairs (VEC = 2)");
+    // dynamic work distribution: pass 1 takes units from work[0], pass 2 from work[1]; each pass
+    // resets the other pass's counter (that launch has completed: same stream)
+    unsigned int *wctr = const_cast<unsigned int *>(&st->work[PASS2 ? 1 : 0]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<DevState *>(st)->work[PASS2 ? 0 : 1] = 0u;
     if (!st->active) return;
     constexpr int VEC = 2;
     constexpr int NO = NDIM - 2;     // outer axes
     constexpr int MA = NO - 1;       // marching axis; axes 0..MA-1 are the side axes
     constexpr int NSA = MA > 0 ? MA : 1;
-    constexpr int RS = R + 2;        // ring slots
+    constexpr int RS = R + NST;      // ring slots
     constexpr bool CT = CN1 > 0;     // shape-specialised instance: geometry known at compile time
     constexpr int NSS = 2 * R * MA;  // side slots per stage
     extern __shared__ __align__(128) float smem[];
@@ -379,13 +384,13 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     const int SSZ = CT ? geo_ssz(CN1, CB) : a.SSZ;
     const int RMG = CT ? geo_rmarg(R, CN1) : a.rmarg;
     float *ring = smem;
-    float *side = smem + (CT ? geo_side_off(R, CN1, CB) : a.side_off);
+    float *side = smem + (CT ? geo_side_off(R, CN1, CB, NST) : a.side_off);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + a.bar_off);
     // tma[b]:   the copies of a step with parity b landed (producer arrive.expect_tx + bytes)
     // empty[b]: every compute warp is done reading that step's buffers (one arrive per warp)
     // gh[k]:    the ghost cells of the centre tile in ring slot k are written (producer arrive);
     //           filled as soon as the tile lands, R steps before it becomes a centre tile
-    uint64_t *tmab = bars, *empty = bars + 2, *gh = bars + 4;
+    uint64_t *tmab = bars, *empty = bars + NST, *gh = bars + 2 * NST, *ubar = bars + 2 * NST + RS;
 
     float mn[NDIM], mx[NDIM], mabs = 0.f;
 #pragma unroll
@@ -438,6 +443,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     long long *t_soff = reinterpret_cast<long long *>(smem + a.tab_off);   // [32]
     uint32_t *t_snb = reinterpret_cast<uint32_t *>(t_soff + 32);           // [32] bytes (0 = skip)
     int *t_ring = reinterpret_cast<int *>(t_snb + 32);                      // [8]
+    int *uq = t_ring + 8;                                                   // [2] unit queue (producer -> compute warps)
     auto make_table = [&](const MarchUnit &U) {
         const int lane = tid & 31;
         int oid[NSA], oN[NSA];
@@ -479,7 +485,8 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     // copies of step `itx` = marching index j of unit U (ring tiles j+kb .. j+R), on tma[itx & 1]
     auto issue = [&](const MarchUnit &U, int j, int itx, int kb) {
         const int lane = tid & 31;
-        uint64_t *bar = &tmab[itx & 1];
+        const int stg = itx % NST;
+        uint64_t *bar = &tmab[stg];
         const long long tj = U.cbase + (long long)(j - mlo) * M;
         uint32_t nb = 0, nbw0 = 0, nbw1 = 0;
         const float *src = nullptr;
@@ -489,7 +496,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
         if (lane < NSS) {
             nb = t_snb[lane];
             src = W + tj + t_soff[lane];
-            dst = smem_u32(side + (itx & 1) * NSS * SSZ + lane * SSZ + MARCH_SMARG);
+            dst = smem_u32(side + stg * NSS * SSZ + lane * SSZ + MARCH_SMARG);
         } else if (lane - NSS >= kb && lane - NSS <= R) {
             const int k = lane - NSS, mj = j + k;
             if (mj < U.m1) {
@@ -551,11 +558,13 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     };
 
     if (tid == 0) {
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NST; ++b) {
             mbar_init(&tmab[b], 1);
             mbar_init(&empty[b], nwc);
         }
         for (int k = 0; k < RS; ++k) mbar_init(&gh[k], 1);
+        mbar_init(&ubar[0], 1);
+        mbar_init(&ubar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -566,7 +575,23 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
         //              (a) when step s's copies have landed, write the ghost cells of the ring
         //                  tiles that came with them (centre tiles R steps later; at a unit's first
         //                  step all R+1) and release them (gh)
-        int u = blockIdx.x;
+        // units are taken from the launch's work counter in order, so the units in flight on the
+        // whole GPU stay a compact range of the L2-friendly work order
+        int nu = 0;                                          // units announced to the compute warps
+        auto grab = [&]() -> int {
+            unsigned int v = 0;
+            if ((tid & 31) == 0) v = atomicAdd(wctr, 1u);
+            v = __shfl_sync(0xffffffffu, v, 0);
+            const int un = v < (unsigned)a.units ? (int)v : -1;
+            if ((tid & 31) == 0) {
+                uq[nu & 1] = un;
+                mbar_arrive(&ubar[nu & 1]);
+            }
+            ++nu;
+            return un;
+        };
+        int u = grab();
+        if (u >= 0) {
         MarchUnit U = march_unit<MA>(a, Nml, mlo, u);
         int jg = U.m0;
         bool first = true;                                   // step sp is the first of its unit
@@ -578,16 +603,17 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
             const bool fresh = jn >= U.m1;
             bool more = true;
             if (fresh) {
-                un = u + gridDim.x;
-                more = un < a.units;
+                un = grab();
+                more = un >= 0;
                 if (more) { Un = march_unit<MA>(a, Nml, mlo, un); jn = Un.m0; }
             }
             if (more) {
-                if (sp >= 1) mbar_wait_sleep(&empty[(sp - 1) & 1], (uint32_t)(((sp - 1) >> 1) & 1));
+                const int sr = sp + 1 - NST;             // the step whose buffers step sp + 1 reuses
+                if (sr >= 0) mbar_wait_sleep(&empty[sr % NST], (uint32_t)((sr / NST) & 1));
                 if (fresh) make_table(Un);
                 issue(Un, jn, sp + 1, fresh ? 0 : R);
             }
-            mbar_wait_sleep(&tmab[sp & 1], (uint32_t)((sp >> 1) & 1));
+            mbar_wait_sleep(&tmab[sp % NST], (uint32_t)((sp / NST) & 1));
 #pragma unroll 1
             for (int k = first ? 0 : R; k <= R; ++k) {
                 if (jg + k >= U.m1) break;
@@ -598,13 +624,18 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
             if (!more) break;
             u = un; U = Un; jg = jn; first = fresh;
         }
+        }
     } else {
         // ================= compute warps =================
         int it = 0;                                      // step counter of this CTA (buffer / phase)
-        int rs0 = 0;                                     // it % RS: ring slot of the current centre tile
+        int rs0 = 0, rph = 0;                            // it % RS (ring slot of the centre tile), (it / RS) & 1
+        int st0 = 0, sph = 0;                            // it % NST (stage), (it / NST) & 1
         const float *rbase = ring + toff;
         const float *sbase = side + sloc;
-        for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+        for (int k = 0;; ++k) {
+            mbar_wait_sleep(&ubar[k & 1], (uint32_t)((k >> 1) & 1));
+            const int u = uq[k & 1];
+            if (u < 0) break;
             const MarchUnit U = march_unit<MA>(a, Nml, mlo, u);
             const int m0 = U.m0, m1 = U.m1;
             const bool act = lrow < U.nrow && tid < a.nthr;
@@ -668,11 +699,11 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                     }
                 }
                 if (!(a.dbg & 1)) {
-                    mbar_wait_sleep(&gh[rs0], (uint32_t)((it / RS) & 1));
-                    mbar_wait_sleep(&tmab[it & 1], (uint32_t)((it >> 1) & 1));
+                    mbar_wait_sleep(&gh[rs0], (uint32_t)rph);
+                    mbar_wait_sleep(&tmab[st0], (uint32_t)sph);
                 }
                 const float *rc = rbase + rs0 * RSZ;                         // this thread's nodes in the centre tile
-                const float *sb = sbase + (it & 1) * (NSS * SSZ);            // ... in side slot 0
+                const float *sb = sbase + st0 * (NSS * SSZ);                 // ... in side slot 0
 
                 if (act && !(a.dbg & 2)) {
                     if (in_ring) vin = *reinterpret_cast<const float2 *>(rbase + (rs0 + R >= RS ? rs0 + R - RS : rs0 + R) * RSZ);
@@ -806,8 +837,9 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                     for (int k = 0; k < R; ++k) win[k] = win[k + 1];
                 }
                 __syncwarp();
-                if ((tid & 31) == 0) mbar_arrive(&empty[it & 1]);   // this warp is done with the step's buffers
-                rs0 = rs0 + 1 == RS ? 0 : rs0 + 1;
+                if ((tid & 31) == 0) mbar_arrive(&empty[st0]);   // this warp is done with the step's buffers
+                if (++rs0 == RS) { rs0 = 0; rph ^= 1; }
+                if (++st0 == NST) { st0 = 0; sph ^= 1; }
             }
         }
     }
@@ -835,10 +867,10 @@ typedef void (*march_fn)(MarchArgs, GridDev, const float *, const float *, const
 // block B in parentheses is what march_plan picks for those shapes).  Any other grid runs the
 // generic instance -- same code, geometry from MarchArgs.
 struct MarchInst {
-    int n1 = 0, b = 0;
+    int n1 = 0, b = 0, nst = 2;
     march_fn pass1 = nullptr, pass2 = nullptr;
 };
-constexpr int MARCH_MAX_INST = 4;
+constexpr int MARCH_MAX_INST = 6;
 struct MarchFnsAll {
     march_fn pass1 = nullptr, pass2 = nullptr;   // generic
     MarchInst inst[MARCH_MAX_INST];
@@ -854,13 +886,13 @@ struct MarchPlan {
     size_t smem = 0;
 };
 
-template <class F, int NDIM, int R, int CN1, int CB>
+template <class F, int NDIM, int R, int CN1, int CB, int NST = 2>
 void march_add(MarchFnsAll &t) {
     if constexpr (NDIM >= 3) {
         MarchInst &m = t.inst[t.ninst++];
-        m.n1 = CN1; m.b = CB;
-        m.pass1 = k_march<F, NDIM, R, 1, false, CN1, CB>;
-        m.pass2 = k_march<F, NDIM, R, 1, true, CN1, CB>;
+        m.n1 = CN1; m.b = CB; m.nst = NST;
+        m.pass1 = k_march<F, NDIM, R, 1, false, CN1, CB, NST>;
+        m.pass2 = k_march<F, NDIM, R, 1, true, CN1, CB, NST>;
     }
 }
 
@@ -873,6 +905,7 @@ MarchFnsAll march_fns() {
         if constexpr (std::is_same<F, FDoubleInt6D>::value) {     // c4 (30^6), c5 (64 x 48^5)
             march_add<F, NDIM, R, 30, 30>(t);
             march_add<F, NDIM, R, 48, 16>(t);
+            if constexpr (R == 2) march_add<F, NDIM, R, 30, 10, 3>(t);    // 3-stage pipeline (experiment)
         } else if constexpr (std::is_same<F, FCar5D>::value && R == 2) {   // c3
             march_add<F, NDIM, R, 40, 20>(t);
         } else if constexpr (std::is_same<F, FCar4D>::value && R == 1) {   // c2
@@ -902,12 +935,14 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     // memory leaves room for 2 CTAs per SM (else 1), the one wasting the fewest rows in the last
     // (ragged) block, the larger on ties
     int best = 0;
+    int nst = 2;
+    if (const char *env = getenv("ODP_MARCH_NST")) nst = std::min(3, std::max(2, atoi(env)));
     for (int pass = 0; pass < 2 && !best; ++pass) {
         const int cap = pass == 0 ? 113 * 1024 : 226 * 1024;
         int best_waste = 1 << 30;
         for (int B = std::min(N2, (MARCH_MAXT1 - 32) / QR); B >= 1; --B) {
             if (B != N2 && (B * N1) % 4) continue;
-            if (geo_smem_bytes(R, N1, B, NSS) > cap) continue;
+            if (geo_smem_bytes(R, N1, B, NSS, nst) > cap) continue;
             const int waste = ((N2 + B - 1) / B) * B - N2;
             if (waste < best_waste) { best_waste = waste; best = B; }
         }
@@ -921,8 +956,13 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     fns->pass2 = all.pass2;
     fns->specialised = 0;
     const bool generic_only = getenv("ODP_MARCH_GENERIC") != nullptr;
+    if (nst != 2) {             // only shape-specialised instances have a 3-stage pipeline
+        bool found = false;
+        for (int i = 0; i < all.ninst; ++i) found |= all.inst[i].n1 == N1 && all.inst[i].b == best && all.inst[i].nst == nst;
+        if (!found) return false;
+    }
     for (int i = 0; i < all.ninst && !generic_only; ++i)
-        if (all.inst[i].n1 == N1 && all.inst[i].b == best) {
+        if (all.inst[i].n1 == N1 && all.inst[i].b == best && all.inst[i].nst == nst) {
             fns->pass1 = all.inst[i].pass1;
             fns->pass2 = all.inst[i].pass2;
             fns->specialised = 1;
@@ -939,9 +979,9 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     a.SSZ = geo_ssz(N1, best);
     a.NSS = NSS;
     a.rmarg = geo_rmarg(R, N1);
-    a.side_off = geo_side_off(R, N1, best);
-    a.bar_off = geo_bar_off(R, N1, best, NSS);
-    a.tab_off = a.bar_off + 16;
+    a.side_off = geo_side_off(R, N1, best, nst);
+    a.bar_off = geo_bar_off(R, N1, best, NSS, nst);
+    a.tab_off = a.bar_off + 32;
     for (int o = 0; o < 3; ++o) a.sn[o] = o < MA ? g.N[o] : 1;
     a.b1 = 1;
     if (MA == 3) {
@@ -966,7 +1006,7 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     a.dbg = 0;
     if (const char *env = getenv("ODP_MARCH_DBG")) a.dbg = atoi(env);
     p->block = ((a.nthr + 31) / 32) * 32 + 32;      // compute warps + the producer warp
-    p->smem = (size_t)geo_smem_bytes(R, N1, best, NSS);
+    p->smem = (size_t)geo_smem_bytes(R, N1, best, NSS, nst);
     p->grid = 0;
     return true;
 }

@@ -219,6 +219,7 @@ __global__ void __launch_bounds__(256) k_finalize(const float *__restrict__ part
 __global__ void k_init_state(DevState *st, double cfl, double eps) {
     st->tau = 0.0; st->tau_target = 0.0; st->eps = eps; st->dt = 0.0; st->cfl = cfl; st->dt_f = 0.f;
     st->maxabs = 0.f; st->nan = 0; st->active = 0; st->status = 0; st->steps = 0; st->stages = 0; st->pending = 0;
+    st->work[0] = st->work[1] = 0u;
     for (int d = 0; d < MAXD; ++d) { st->minD[d] = 0.f; st->maxD[d] = 0.f; st->amax[d] = 0.f; }
 }
 
@@ -239,6 +240,7 @@ __global__ void k_force_active(DevState *st) {
 // (same float64 expression); k_guard checks the stage OUTPUT (= the next stage's input) from the
 // max|V| / NaN partials pass 2 wrote, and counts the stage.
 __global__ void k_dt(DevState *st, const double *__restrict__ dxd, int n) {
+    st->work[1] = 0u;              // the previous launch may have been a pass 2 (k_march work counters)
     if (!st->active) return;
     if (st->pending) { st->status = ODP_ENUMERIC; st->active = 0; return; }   // detected at this stage's input
     double sum = 0.0;                                                 // Alg. 2 l.167
@@ -285,6 +287,7 @@ __global__ void __launch_bounds__(256) k_guard(const float *__restrict__ partial
             else { st->status = ODP_ENUMERIC; st->active = 0; }
         }
         st->maxabs = ma;
+        st->work[1] = 0u;          // single-pass: pass 2 follows pass 2 (see k_march's work counters)
     }
 }
 

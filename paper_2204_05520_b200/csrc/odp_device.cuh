@@ -49,6 +49,7 @@ struct DevState {
     int active;          // 1 while the current save interval still needs steps
     int status;          // 0 ok, 2 numeric failure (A19)
     int pending;         // single-pass: the last stage's OUTPUT failed the guard; fail at the next stage's start
+    unsigned int work[2];  // dynamic work counters of the march pass-1 / pass-2 launches (each resets the other's)
     long long steps, stages;
 };
 
