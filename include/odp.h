@@ -50,14 +50,17 @@ typedef enum { ODP_BRS = 0, ODP_BRT = 1 } odp_mode;
  *   DUBINS3D       [v, wbar, goal]             (x, y, th): v cos th, v sin th, w
  *   CAR4D          [abar, wbar, dxbar, dybar, goal]  (x, y, v, th): v cos th + dx, v sin th + dy, a, w
  *   CAR5D          [abar, alphabar, goal]      (x, y, th, v, w): v cos th, v sin th, w, a, alpha
- *   DOUBLEINT6D    [ubar, dbar, goal]          (px, vx, py, vy, pz, vz): v_i, u_i + d_i        */
+ *   DOUBLEINT6D    [ubar, dbar, goal]          (px, vx, py, vy, pz, vz): v_i, u_i + d_i
+ *   PAIR_DUBINS3D  [va, vb, abar, bbar, goal]  (x, y, th): -va + vb cos th + a y, va sin th - a x, b - a;
+ *                  a (evader) takes the goal's extremum, b (pursuer) the opposite (reading A30) */
 typedef enum {
     ODP_DYN_HOLONOMIC_BALL = 0,
     ODP_DYN_HOLONOMIC_BOX = 1,
     ODP_DYN_DUBINS3D = 2,
     ODP_DYN_CAR4D = 3,
     ODP_DYN_CAR5D = 4,
-    ODP_DYN_DOUBLEINT6D = 5
+    ODP_DYN_DOUBLEINT6D = 5,
+    ODP_DYN_PAIR_DUBINS3D = 6   /* Eq. 7, the paper's own 3D example */
 } odp_dynamics;
 
 /* Kernel family used for the two passes of every stage. */

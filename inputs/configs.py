@@ -92,8 +92,18 @@ C5_LOW = Workload(
     accuracy="low", cfl=0.8, mode="brt", target=("sphere", (0, 2, 4), 1.0),
     note="6D at scale (65 GB per array): 2/4/8 GPUs only")
 C5_MED = replace(C5_LOW, name="c5-med", accuracy="medium", cfl=0.5)
+# the paper's own 3D example, Eq. 7, at Table 1's 3D shape 100^3.
+# The paper gives neither speeds, input bounds, domain nor target; reading A30 takes the classic
+# pursuit-evasion setting of that system: va = vb = 5, |a|, |b| <= 1, capture radius 5,
+# x in [-6, 20], y in [-10, 10], th in [-pi, pi) periodic, horizon 2.8; the evader (a) avoids
+# (goal +1, maximise), the pursuer (b) does the opposite.  First order (Table 1's "1st order ENO").
+F2 = Workload(
+    name="f2", N=(100, 100, 100), lo=(-6.0, -10.0, -PI), hi=(20.0, 10.0, PI), periodic=(0, 0, 1),
+    dynamics="PAIR_DUBINS3D", params=(5.0, 5.0, 1.0, 1.0, +1.0), tau=(0.0, 2.8),
+    accuracy="low", cfl=0.8, mode="brt", target=("cylinder", (0, 1), 5.0),
+    note="Eq. 7 pairwise Dubins capture (reading A30), 100^3, upwind + Euler")
 
-CONFIGS = {w.name: w for w in (C1, C2, C3, C4, C5_LOW, C5_MED)}
+CONFIGS = {w.name: w for w in (C1, C2, C3, C4, C5_LOW, C5_MED, F2)}
 
 
 def axis_nodes(N: int, lo: float, hi: float, periodic: bool) -> np.ndarray:

@@ -23,7 +23,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "odp_oracle.c")
 _LIB = os.path.join(_HERE, "libodp_oracle.so")
 
-DYN_IDS = {"HOLONOMIC_BALL": 0, "HOLONOMIC_BOX": 1, "DUBINS3D": 2, "CAR4D": 3, "CAR5D": 4, "DOUBLEINT6D": 5}
+DYN_IDS = {"HOLONOMIC_BALL": 0, "HOLONOMIC_BOX": 1, "DUBINS3D": 2, "CAR4D": 3, "CAR5D": 4, "DOUBLEINT6D": 5,
+           "PAIR_DUBINS3D": 6}
 ACC_IDS = {"low": 1, "medium": 2}
 MODE_IDS = {"brs": 0, "brt": 1}
 OK, EINVAL, ENUMERIC, ENOMEM = 0, 1, 2, 5

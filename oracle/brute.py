@@ -98,6 +98,11 @@ def model(dyn, params, n):
         ub, db = p[:2]
         f = lambda X, u, d: [X[1], u[0] + d[0] + 0.0 * X[0], X[3], u[1] + d[1] + 0.0 * X[0], X[5], u[2] + d[2] + 0.0 * X[0]]
         return f, list(itertools.product(*[(-ub, ub)] * 3)), list(itertools.product(*[(-db, db)] * 3)), goal, None
+    if dyn == "PAIR_DUBINS3D":      # Eq. 7: u = a (evader), d = b (pursuer)
+        va, vb, ab, bb = p[:4]
+        f = lambda X, u, d: [-va + vb * np.cos(X[2]) + u[0] * X[1], va * np.sin(X[2]) - u[0] * X[0],
+                             d[0] - u[0] + 0.0 * X[0]]
+        return f, [(-ab,), (ab,)], [(-bb,), (bb,)], goal, None
     raise ValueError(dyn)
 
 
@@ -138,6 +143,24 @@ def alpha(dyn, params, X, minD, maxD):
                 if e != d and not (minD[e] <= 0 <= maxD[e]):
                     den += min(abs(minD[e]), abs(maxD[e])) ** 2
             out.append(np.full(shape, ball * Md / math.sqrt(den)))
+        return out
+    if dyn == "PAIR_DUBINS3D":
+        # the switching function q = p_x y - p_y x - p_th is linear in p: its range over the costate
+        # box is attained at the box corners (enumerated here); b* follows sgn(p_th)   (A30)
+        va, vb, ab, bb = list(params)[:4]
+        corners = list(itertools.product((minD[0], maxD[0]), (minD[1], maxD[1]), (minD[2], maxD[2])))
+        qs = [c[0] * X[1] - c[1] * X[0] - c[2] for c in corners]
+        qlo = np.minimum.reduce([np.broadcast_to(q, shape) for q in qs])
+        qhi = np.maximum.reduce([np.broadcast_to(q, shape) for q in qs])
+        out = [np.zeros(shape) for _ in range(n)]
+        st = ([1.0] if maxD[2] >= 0 else []) + ([-1.0] if minD[2] < 0 else [])
+        for sq, mask in ((1.0, qhi >= 0), (-1.0, qlo < 0)):
+            a = goal * ab * sq
+            for sb in st:
+                b = -goal * bb * sb
+                fx = f(X, (a,), (b,))
+                for k in range(n):
+                    out[k] = np.where(mask, np.maximum(out[k], np.abs(np.broadcast_to(fx[k], shape))), out[k])
         return out
     signsets = []
     for d in range(n):

@@ -28,6 +28,9 @@
  *   A13 ENO2 with second differences, tie |a| <= |b| picks the left candidate.
  *   A14 bang-bang sgn(0) = +1.    A15 periodic axes exclude the upper endpoint.
  *   A19 NaN or max|V| > 1e10 is a numerical failure.   A20 all alpha^max = 0 -> dt = tau_k - tau.
+ *   A30 Eq. 7 (pairwise Dubins): evader control a (|a| <= abar, the goal's extremum),
+ *       pursuer b (|b| <= bbar, the opposite); alpha over the sign set of q = p_x y - p_y x - p_th
+ *       (its range over the costate box, linear in p) and, for the th axis, of p_th independently.
  */
 #include <math.h>
 #include <stdint.h>
@@ -44,7 +47,8 @@
 #define OR_ENOMEM 5
 
 /* oracle-local dynamics identifiers (mapped from names by oracle/__init__.py) */
-enum { OR_HOLO_BALL = 0, OR_HOLO_BOX = 1, OR_DUBINS3D = 2, OR_CAR4D = 3, OR_CAR5D = 4, OR_DOUBLEINT6D = 5 };
+enum { OR_HOLO_BALL = 0, OR_HOLO_BOX = 1, OR_DUBINS3D = 2, OR_CAR4D = 3, OR_CAR5D = 4, OR_DOUBLEINT6D = 5,
+       OR_PAIR_DUBINS3D = 6 };
 enum { OR_LOW = 1, OR_MEDIUM = 2 };
 enum { OR_BRS = 0, OR_BRT = 1 };
 
@@ -145,9 +149,9 @@ static void og_deriv(const og *g, const double *W, const int64_t *idx, int64_t f
 typedef struct { int id, n; double prm[8]; } ofun;
 
 static int of_init(ofun *f, int id, int n, const double *prm, int np) {
-    static const int want_np[6] = {2, 3, 3, 5, 3, 3};
-    static const int want_n[6] = {0, 0, 3, 4, 5, 6};
-    if (id < 0 || id > 5) return OR_EINVAL;
+    static const int want_np[7] = {2, 3, 3, 5, 3, 3, 5};
+    static const int want_n[7] = {0, 0, 3, 4, 5, 6, 3};
+    if (id < 0 || id > 6) return OR_EINVAL;
     if (np != want_np[id]) return OR_EINVAL;
     if (want_n[id] != 0 && n != want_n[id]) return OR_EINVAL;
     if (n < 1 || n > 6) return OR_EINVAL;
@@ -191,6 +195,11 @@ static void of_opt(const ofun *f, const double *x, const double *p, double *u, d
             dd[i] = -c[2] * c[1] * sgn1(p[2 * i + 1]);
         }
         break;
+    case OR_PAIR_DUBINS3D: /* Eq. 7, [va, vb, abar, bbar, goal]; u = a (evader), d = b (pursuer)
+                            * p.f = p_x(-va + vb cos th) + p_y va sin th + a (p_x y - p_y x - p_th) + b p_th */
+        u[0] = c[4] * c[2] * sgn1(p[0] * x[1] - p[1] * x[0] - p[2]);
+        dd[0] = -c[4] * c[3] * sgn1(p[2]);
+        break;
     }
 }
 
@@ -227,6 +236,11 @@ static void of_rate(const ofun *f, const double *x, const double *u, const doubl
             fx[2 * i] = x[2 * i + 1];
             fx[2 * i + 1] = u[i] + dd[i];
         }
+        break;
+    case OR_PAIR_DUBINS3D: /* Eq. 7: relative (x, y, th) of pursuer b w.r.t. evader a */
+        fx[0] = -c[0] + c[1] * cos(x[2]) + u[0] * x[1];
+        fx[1] = c[0] * sin(x[2]) - u[0] * x[0];
+        fx[2] = dd[0] - u[0];
         break;
     }
 }
@@ -291,6 +305,27 @@ static double of_alpha(const ofun *f, const double *x, int d, const double *minD
         k = sign_set(minD[d], maxD[d], s);
         for (int j = 0; j < k; ++j) best = fmax(best, fabs(c[2] * c[0] * s[j] - c[2] * c[1] * s[j]));
         return best;
+    case OR_PAIR_DUBINS3D: {
+        /* a* = goal abar sgn(q), q = p_x y - p_y x - p_th; b* = -goal bbar sgn(p_th) (A30).  The
+         * range of q over the costate box is the sum of the ranges of its three terms (it is linear
+         * in p); alpha takes the maximum over the sign set of q and, for d = th, the sign set of
+         * p_th independently (an outer bound of the joint sign set, exact when both sets hold both
+         * signs, reading A30). */
+        double qlo = 0.0, qhi = 0.0;
+        const double cx = x[1], cy = -x[0];               /* q = cx p_x + cy p_y - p_th */
+        qlo += fmin(cx * minD[0], cx * maxD[0]); qhi += fmax(cx * minD[0], cx * maxD[0]);
+        qlo += fmin(cy * minD[1], cy * maxD[1]); qhi += fmax(cy * minD[1], cy * maxD[1]);
+        qlo += -maxD[2]; qhi += -minD[2];
+        double sq[2], st[2];
+        const int kq = sign_set(qlo, qhi, sq), kt = sign_set(minD[2], maxD[2], st);
+        for (int j = 0; j < kq; ++j) {
+            const double a = c[4] * c[2] * sq[j];
+            if (d == 0) best = fmax(best, fabs(-c[0] + c[1] * cos(x[2]) + a * x[1]));
+            else if (d == 1) best = fmax(best, fabs(c[0] * sin(x[2]) - a * x[0]));
+            else
+                for (int i = 0; i < kt; ++i) best = fmax(best, fabs(-c[4] * c[3] * st[i] - a));
+        }
+        return best; }
     }
     return 0.0;
 }

@@ -18,7 +18,8 @@ ODP_OK, ODP_EINVAL, ODP_ENUMERIC, ODP_ECUDA, ODP_ENCCL, ODP_ENOMEM = 0, 1, 2, 3,
 ACCURACY = {"low": 1, "medium": 2}
 MODE = {"brs": 0, "brt": 1}
 KERNEL = {"auto": 0, "generic": 1, "tiled": 2, "stream": 3, "march": 4}
-DYNAMICS = {"HOLONOMIC_BALL": 0, "HOLONOMIC_BOX": 1, "DUBINS3D": 2, "CAR4D": 3, "CAR5D": 4, "DOUBLEINT6D": 5}
+DYNAMICS = {"HOLONOMIC_BALL": 0, "HOLONOMIC_BOX": 1, "DUBINS3D": 2, "CAR4D": 3, "CAR5D": 4, "DOUBLEINT6D": 5,
+            "PAIR_DUBINS3D": 6}
 
 # every symbol include/odp.h declares (checked by tests/test_capi_host.py)
 EXPORTS = ("odp_grid_create", "odp_grid_destroy", "odp_grid_info", "odp_hj_solve", "odp_hj_solve_host",

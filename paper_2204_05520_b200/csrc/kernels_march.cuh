@@ -53,6 +53,9 @@ namespace odp {
 #ifndef ODP_MARCH_MINB2
 #define ODP_MARCH_MINB2 1      // ... and of the NP=2 (VEC=4) kernels
 #endif
+#ifndef ODP_MARCH_WAIT
+#define ODP_MARCH_WAIT 1       // 1: mbarrier try_wait with a suspend hint; 0: try_wait + nanosleep back-off
+#endif
 #ifndef ODP_MARCH_SELP
 #define ODP_MARCH_SELP 0       // 1: ENO pick as FSET + 3 FMA-pipe ops instead of FSETP + FSEL
 #endif
@@ -116,6 +119,13 @@ __device__ __forceinline__ void inc_val(float2 v, float &mn, float &mx) {
 __device__ __forceinline__ void inc_s(float v, float &mn, float &mx) {
     mn = fminf(mn, v);
     mx = fmaxf(mx, v);
+}
+
+// 8-byte shared-memory load at a 32-bit shared address (one base register + immediate offsets)
+__device__ __forceinline__ float2 lds2(uint32_t addr) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -218,9 +228,11 @@ template <> struct Terms<FDoubleInt6D> { static constexpr unsigned LIN = 0x15, A
 
 template <class F>
 __device__ __forceinline__ void axis_terms(const F &f, int d, const Pt &q0, const Pt &q1, float hih, float2 u,
-                                           float2 w, float2 &acc, float2 &dis) {
+                                           float2 w, float2 &acc, float2 &dis, float2 *pv) {
     const float2 s = add2(u, w), t = sub2(w, u);
-    if constexpr (Sep<F>::ball) {
+    if constexpr (!F::SEPARABLE) {
+        pv[d] = mul2(s, f2s(hih));                   // p_d = (D- + D+)/2 (A3); H at the end of the node
+    } else if constexpr (Sep<F>::ball) {
         const float2 sh = mul2(s, f2s(hih));
         acc = fma2(sh, sh, acc);
     } else {
@@ -238,6 +250,9 @@ __device__ __forceinline__ float2 ham_fin2(const F &f, float2 acc) {
     if constexpr (Sep<F>::ball) return f2(f.kH * sqrtf(acc.x), f.kH * sqrtf(acc.y));
     else return acc;
 }
+template <> struct Terms<FPairDubins3D> { static constexpr unsigned LIN = 0, ABS = 0; };
+__device__ __forceinline__ float lin_c(const FPairDubins3D &, int, const Pt &) { return 0.f; }
+__device__ __forceinline__ float abs_k(const FPairDubins3D &, int) { return 0.f; }
 
 // ---- kernel -------------------------------------------------------------------------------------
 //
@@ -269,7 +284,7 @@ struct MarchArgs {
     int sn[3];            // local extents of the side axes (work order, march_col)
     int b1;               // axis-1 block of the work order (divides sn[1])
     int ncols;            // columns (product of the side extents)
-    int dbg;              // experiments only (ODP_MARCH_DBG): 1 = skip the data waits, 2 = skip the arithmetic
+    int dbg;              // experiments only (ODP_MARCH_DBG): 2 = skip the arithmetic, 4 = skip the copies
     int K, nseg, units;   // marching segment length, segments per column, work units
 };
 constexpr int MARCH_SMARG = 4;   // leading margin of a side slot (floats)
@@ -344,6 +359,10 @@ __device__ __forceinline__ MarchUnit march_unit(const MarchArgs &a, int Nml, int
 // mbarrier wait with back-off: a warp that finds its data missing sleeps instead of spinning, so
 // it does not take issue slots from the warps that are computing
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+#if ODP_MARCH_WAIT == 1
+    mbar_wait(bar, parity);      // try_wait with a suspend-time hint: the hardware parks the warp
+    return;
+#endif
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -509,6 +528,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                 nbw1 = (uint32_t)t_ring[4];
             }
         }
+        if (a.dbg & 4) nb = nbw0 = nbw1 = 0;          // experiment: no data movement (garbage tiles)
         const uint32_t total = __reduce_add_sync(0xffffffffu, nb + nbw0 + nbw1);
         if (lane == 0) mbar_expect_tx(bar, total);
         __syncwarp();
@@ -617,7 +637,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
 #pragma unroll 1
             for (int k = first ? 0 : R; k <= R; ++k) {
                 if (jg + k >= U.m1) break;
-                fill_ghosts(U, (sp + k) % RS);
+                if (!(a.dbg & 8)) fill_ghosts(U, (sp + k) % RS);
                 __syncwarp();
                 if ((tid & 31) == 0) mbar_arrive(&gh[(sp + k) % RS]);
             }
@@ -630,8 +650,10 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
         int it = 0;                                      // step counter of this CTA (buffer / phase)
         int rs0 = 0, rph = 0;                            // it % RS (ring slot of the centre tile), (it / RS) & 1
         int st0 = 0, sph = 0;                            // it % NST (stage), (it / NST) & 1
-        const float *rbase = ring + toff;
-        const float *sbase = side + sloc;
+        const uint32_t rb_s = smem_u32(ring + toff);    // this thread's nodes in ring slot 0 (bytes)
+        const uint32_t sb_s = smem_u32(side + sloc);    // ... in side slot 0 of stage 0
+        const uint32_t lof = 4u * (uint32_t)loff, rof = 4u * (uint32_t)roff;
+        int rsw = R;                                     // (it + R) % RS: ring slot of the entering window tile
         for (int k = 0;; ++k) {
             mbar_wait_sleep(&ubar[k & 1], (uint32_t)((k >> 1) & 1));
             const int u = uq[k & 1];
@@ -682,9 +704,8 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                 }
             }
 
-            for (int jg = m0; jg < m1; ++jg, ++it) {
-                const int jl = jg - mlo;
-                const long long gi = U.cbase + (long long)jl * M + grow * N1 + qc0;   // element of node 0
+            long long gi = U.cbase + (long long)(m0 - mlo) * M + grow * N1 + qc0;   // element of node 0 (this step)
+            for (int jg = m0; jg < m1; ++jg, ++it, gi += M) {
                 // window value entering at this step: v_{j+R} (ring inside the segment, else global / ghost)
                 const int kin = jg + R;
                 const bool in_ring = kin < m1;
@@ -698,15 +719,13 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                         vin = ghost2(e, in, (float)(kin - Nm + 1));
                     }
                 }
-                if (!(a.dbg & 1)) {
-                    mbar_wait_sleep(&gh[rs0], (uint32_t)rph);
-                    mbar_wait_sleep(&tmab[st0], (uint32_t)sph);
-                }
-                const float *rc = rbase + rs0 * RSZ;                         // this thread's nodes in the centre tile
-                const float *sb = sbase + st0 * (NSS * SSZ);                 // ... in side slot 0
+                mbar_wait_sleep(&gh[rs0], (uint32_t)rph);
+                mbar_wait_sleep(&tmab[st0], (uint32_t)sph);
+                const uint32_t rcs = rb_s + (uint32_t)(rs0 * RSZ * 4);      // this thread's nodes in the centre tile
+                const uint32_t sbs = sb_s + (uint32_t)(st0 * NSS * SSZ * 4); // ... in side slot 0
 
                 if (act && !(a.dbg & 2)) {
-                    if (in_ring) vin = *reinterpret_cast<const float2 *>(rbase + (rs0 + R >= RS ? rs0 + R - RS : rs0 + R) * RSZ);
+                    if (in_ring) vin = lds2(rb_s + (uint32_t)(rsw * RSZ * 4));
                     win[R] = vin;
                     const float2 v0 = win[0];
                     Pt q0;
@@ -715,11 +734,16 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                         load_axis<F>(g, q0, MA, jg);
                     }
                     float2 acc = f2s(0.f), dis = f2s(0.f);
-                    auto terms = [&](int d, float2 uu, float2 ww) {
-                        Pt a0 = q0, a1 = q0;
+                    float2 pv[F::SEPARABLE ? 1 : NDIM];     // costate of the node pair (non-separable H)
+                    auto node_pts = [&](Pt &a0, Pt &a1) {
+                        a0 = q0; a1 = q0;
                         a0.x[NDIM - 1] = qcv[0].x[NDIM - 1]; a0.c[NDIM - 1] = qcv[0].c[NDIM - 1]; a0.s[NDIM - 1] = qcv[0].s[NDIM - 1];
                         a1.x[NDIM - 1] = qcv[1].x[NDIM - 1]; a1.c[NDIM - 1] = qcv[1].c[NDIM - 1]; a1.s[NDIM - 1] = qcv[1].s[NDIM - 1];
-                        axis_terms(f, d, a0, a1, hih[d], uu, ww, acc, dis);
+                    };
+                    auto terms = [&](int d, float2 uu, float2 ww) {
+                        Pt a0, a1;
+                        node_pts(a0, a1);
+                        axis_terms(f, d, a0, a1, hih[d], uu, ww, acc, dis, pv);
                     };
                     // one-sided derivatives of a full window x[0..2R] (classic): h D-, h D+
                     auto classic = [&](const float2 *x, float2 &uu, float2 &ww, float2 &mr, float2 &d1r) {
@@ -758,12 +782,12 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                     // ---- side axes (CTA-uniform faces), neighbours from the side slots ----
 #pragma unroll
                     for (int o = 0; o < MA; ++o) {
-                        const float *so = sb + (o * 2 * R) * SSZ;
+                        const uint32_t so = sbs + (uint32_t)(o * 2 * R * SSZ * 4);
                         if (PASS2 || oface[o]) {
                             float2 x[2 * R + 1];
 #pragma unroll
                             for (int k = -R; k <= R; ++k)
-                                x[k + R] = k == 0 ? v0 : *reinterpret_cast<const float2 *>(so + (k < 0 ? k + R : k + R - 1) * SSZ);
+                                x[k + R] = k == 0 ? v0 : lds2(so + (uint32_t)((k < 0 ? k + R : k + R - 1) * SSZ * 4));
                             if (oface[o]) fix_ghosts2<R>(x, oid[o], oN[o]);
                             float2 uu, ww, mr, d1r;
                             classic(x, uu, ww, mr, d1r);
@@ -777,12 +801,12 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                         } else {
                             // pass 1, interior: the node's upper edge i+1/2 (both sides)
                             if constexpr (R == 2) {
-                                const float2 s1 = *reinterpret_cast<const float2 *>(so + 1 * SSZ);
-                                const float2 s2 = *reinterpret_cast<const float2 *>(so + 2 * SSZ);
-                                const float2 s3 = *reinterpret_cast<const float2 *>(so + 3 * SSZ);
+                                const float2 s1 = lds2(so + (uint32_t)(1 * SSZ * 4));
+                                const float2 s2 = lds2(so + (uint32_t)(2 * SSZ * 4));
+                                const float2 s3 = lds2(so + (uint32_t)(3 * SSZ * 4));
                                 inc_edge(pick2(d2p(s1, v0, s2), d2p(v0, s2, s3)), sub2(s2, v0), mn[o], mx[o]);
                             } else {
-                                inc_val(sub2(*reinterpret_cast<const float2 *>(so + 1 * SSZ), v0), mn[o], mx[o]);
+                                inc_val(sub2(lds2(so + (uint32_t)(1 * SSZ * 4)), v0), mn[o], mx[o]);
                             }
                         }
                     }
@@ -791,7 +815,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                     {
                         float2 x[2 * R + 1];
 #pragma unroll
-                        for (int k = -R; k <= R; ++k) x[k + R] = k == 0 ? v0 : *reinterpret_cast<const float2 *>(rc + k * N1);
+                        for (int k = -R; k <= R; ++k) x[k + R] = k == 0 ? v0 : lds2(rcs + (uint32_t)(k * N1 * 4));
                         float2 uu, ww, mr, d1r;
                         classic(x, uu, ww, mr, d1r);
                         if constexpr (PASS2) terms(NDIM - 2, uu, ww);
@@ -800,8 +824,8 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
 
                     // ---- in-plane columns (axis n-1): left / right pairs (tile or ghost table) ----
                     {
-                        const float2 lp = *reinterpret_cast<const float2 *>(rc + loff);
-                        const float2 rp = *reinterpret_cast<const float2 *>(rc + roff);
+                        const float2 lp = lds2(rcs + lof);
+                        const float2 rp = lds2(rcs + rof);
                         float2 uu, ww;
                         if constexpr (R == 2) {
                             // columns -2 -1 | 0 1 | 2 3 ; second differences at -1 0 1 2 ; edges -1/2, 1/2, 3/2
@@ -820,6 +844,14 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                     }
 
                     if constexpr (PASS2) {
+                        if constexpr (!F::SEPARABLE) {             // H = p.f(x, u*, d*) per node (Alg. 2 l.154-156)
+                            Pt a0, a1;
+                            node_pts(a0, a1);
+                            float p0[NDIM], p1[NDIM];
+#pragma unroll
+                            for (int d = 0; d < NDIM; ++d) { p0[d] = pv[d].x; p1[d] = pv[d].y; }
+                            acc = f2(f.ham(a0, p0), f.ham(a1, p1));
+                        }
                         const float2 L = add2(ham_fin2(f, acc), dis);
                         float2 v = fma2(f2s(dt), L, v0);                        // W + dt L
                         if (kind == STAGE_RK2) v = mul2(f2s(0.5f), add2(vnv, v));  // (Vn + V2)/2 (A10)
@@ -839,6 +871,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                 __syncwarp();
                 if ((tid & 31) == 0) mbar_arrive(&empty[st0]);   // this warp is done with the step's buffers
                 if (++rs0 == RS) { rs0 = 0; rph ^= 1; }
+                if (++rsw == RS) rsw = 0;
                 if (++st0 == NST) { st0 = 0; sph ^= 1; }
             }
         }
@@ -905,7 +938,7 @@ MarchFnsAll march_fns() {
         if constexpr (std::is_same<F, FDoubleInt6D>::value) {     // c4 (30^6), c5 (64 x 48^5)
             march_add<F, NDIM, R, 30, 30>(t);
             march_add<F, NDIM, R, 48, 16>(t);
-            if constexpr (R == 2) march_add<F, NDIM, R, 30, 10, 3>(t);    // 3-stage pipeline (experiment)
+            if constexpr (R == 2) march_add<F, NDIM, R, 30, 30, 3>(t);    // 3-stage pipeline, 1 CTA/SM (experiment)
         } else if constexpr (std::is_same<F, FCar5D>::value && R == 2) {   // c3
             march_add<F, NDIM, R, 40, 20>(t);
         } else if constexpr (std::is_same<F, FCar4D>::value && R == 1) {   // c2
@@ -937,7 +970,8 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     int best = 0;
     int nst = 2;
     if (const char *env = getenv("ODP_MARCH_NST")) nst = std::min(3, std::max(2, atoi(env)));
-    for (int pass = 0; pass < 2 && !best; ++pass) {
+    const bool one_cta = getenv("ODP_MARCH_1CTA") != nullptr;
+    for (int pass = one_cta ? 1 : 0; pass < 2 && !best; ++pass) {
         const int cap = pass == 0 ? 113 * 1024 : 226 * 1024;
         int best_waste = 1 << 30;
         for (int B = std::min(N2, (MARCH_MAXT1 - 32) / QR); B >= 1; --B) {

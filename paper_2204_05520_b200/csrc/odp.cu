@@ -133,7 +133,8 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const float *__restrict
 template <class F, int NDIM>
 __global__ void __launch_bounds__(256) k_finalize(const float *__restrict__ partials, int nparts, DevState *st,
                                                   GridDev g, FParams fp, const double *__restrict__ dxd,
-                                                  int stage_in_step, int final_check, const float *__restrict__ range) {
+                                                  int stage_in_step, int final_check, const float *__restrict__ range,
+                                                  const float *__restrict__ amax_parts, int namax) {
     if (!st->active) return;
     constexpr int Q = 2 * NDIM + 2;
     __shared__ float red[Q][8];
@@ -182,6 +183,14 @@ __global__ void __launch_bounds__(256) k_finalize(const float *__restrict__ part
     F f;
     f.init(fp, rng, rng + NDIM);
     __shared__ float am[NDIM];
+    if constexpr (F::DEPS3) {   // alpha_d depends on 3 coordinates: per-CTA maxima from k_amax3
+        if (threadIdx.x < NDIM) {
+            float a = 0.f;
+            for (int p = 0; p < namax; ++p) a = fmaxf(a, amax_parts[p * NDIM + threadIdx.x]);
+            am[threadIdx.x] = a;
+        }
+        __syncthreads();
+    } else
     for (int d = 0; d < NDIM; ++d) {
         const int m = F::deps(d);
         int ax[2] = {-1, -1}, na = 0;
@@ -232,6 +241,80 @@ __global__ void k_begin(DevState *st, double tau_k) {
 __global__ void k_force_active(DevState *st) {
     if (st->pending) { st->status = ODP_ENUMERIC; st->pending = 0; }
     st->active = st->status == 0 ? 1 : 0;
+}
+
+// For functors whose alpha_d depends on three coordinates (DEPS3, e.g. Eq. 7): the stage's range is
+// stored first (k_store_range: the same exact min/max reduction as k_finalize), then k_amax3 takes
+// the maximum of alpha_{i,d} over the nodes of that coordinate grid with many CTAs (the
+// one-CTA enumeration of k_finalize would cost N0 N1 N2 / 256 iterations per stage).
+template <int NDIM>
+__global__ void __launch_bounds__(256) k_store_range(const float *__restrict__ partials, int nparts, DevState *st,
+                                                     const float *__restrict__ range) {
+    if (!st->active) return;
+    constexpr int Q = 2 * NDIM + 2;
+    __shared__ float red[Q][8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (range) {
+        if (threadIdx.x < NDIM) { st->minD[threadIdx.x] = -range[threadIdx.x]; st->maxD[threadIdx.x] = range[NDIM + threadIdx.x]; }
+        return;
+    }
+    for (int q = 0; q < 2 * NDIM; ++q) {
+        float r = q < NDIM ? __int_as_float(0x7f800000) : -__int_as_float(0x7f800000);
+        for (int p = threadIdx.x; p < nparts; p += blockDim.x) {
+            const float o = partials[(long long)p * Q + q];
+            r = q < NDIM ? fminf(r, o) : fmaxf(r, o);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const float o = __shfl_xor_sync(0xffffffffu, r, off);
+            r = q < NDIM ? fminf(r, o) : fmaxf(r, o);
+        }
+        if (lane == 0) red[q][warp] = r;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * NDIM) {
+        const int q = threadIdx.x;
+        float r = red[q][0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = q < NDIM ? fminf(r, red[q][w]) : fmaxf(r, red[q][w]);
+        if (q < NDIM) st->minD[q] = r; else st->maxD[q - NDIM] = r;
+    }
+}
+
+template <class F, int NDIM>
+__global__ void __launch_bounds__(256) k_amax3(GridDev g, FParams fp, const DevState *st, float *parts) {
+    if (!st->active) return;
+    F f;
+    f.init(fp, st->minD, st->maxD);
+    float a[NDIM];
+#pragma unroll
+    for (int d = 0; d < NDIM; ++d) a[d] = 0.f;
+    const long long n = (long long)g.Ng[0] * g.Ng[1] * g.Ng[2];
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int i2 = (int)(i % g.Ng[2]);
+        const long long r = i / g.Ng[2];
+        const int i1 = (int)(r % g.Ng[1]), i0 = (int)(r / g.Ng[1]);
+        Pt q;
+        load_axis<F>(g, q, 0, i0);
+        load_axis<F>(g, q, 1, i1);
+        load_axis<F>(g, q, 2, i2);
+#pragma unroll
+        for (int d = 0; d < NDIM; ++d) a[d] = fmaxf(a[d], f.alpha(d, q));
+    }
+    __shared__ float red[NDIM][8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 0; d < NDIM; ++d) {
+        float r = a[d];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) r = fmaxf(r, __shfl_xor_sync(0xffffffffu, r, off));
+        if (lane == 0) red[d][warp] = r;
+    }
+    __syncthreads();
+    if (threadIdx.x < NDIM) {
+        float r = red[threadIdx.x][0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = fmaxf(r, red[threadIdx.x][w]);
+        parts[blockIdx.x * NDIM + threadIdx.x] = r;
+    }
 }
 
 // Single-pass solves: for a functor whose alpha_(i,d) does not depend on the
@@ -304,7 +387,10 @@ __global__ void k_advance(DevState *st) {                               // O8: t
 typedef void (*pass1_fn)(GridDev, const float *, float *, const DevState *);
 typedef void (*pass2_fn)(GridDev, const float *, const float *, const float *, float *, const DevState *, FParams,
                          int, int);
-typedef void (*fin_fn)(const float *, int, DevState *, GridDev, FParams, const double *, int, int, const float *);
+typedef void (*fin_fn)(const float *, int, DevState *, GridDev, FParams, const double *, int, int, const float *,
+                       const float *, int);
+typedef void (*srange_fn)(const float *, int, DevState *, const float *);
+typedef void (*amax3_fn)(GridDev, FParams, const DevState *, float *);
 typedef void (*red_fn)(const float *, int, const DevState *, float *);
 typedef void (*guard_fn)(const float *, int, DevState *, const float *, int);
 
@@ -314,6 +400,8 @@ struct KernelSet {
     fin_fn fin = nullptr;
     red_fn red = nullptr;
     guard_fn guard = nullptr;
+    srange_fn srange = nullptr;   // DEPS3 functors only
+    amax3_fn amax3 = nullptr;
     bool range_free = false;
     TiledFns tiled;      // tiled family (may be empty)
     StreamFnsAll stream; // stream family (may be empty)
@@ -329,8 +417,14 @@ static KernelSet make_set() {
     k.red = k_reduce_partials<NDIM>;
     k.guard = k_guard<NDIM>;
     k.range_free = F::RANGE_FREE;
-    k.tiled = tiled_fns<F, NDIM, R>();
-    k.stream = stream_fns<F, NDIM, R>();
+    if constexpr (F::DEPS3) {
+        k.srange = k_store_range<NDIM>;
+        k.amax3 = k_amax3<F, NDIM>;
+    }
+    if constexpr (F::SEPARABLE) {      // the tiled / stream families assemble separable Hamiltonians only
+        k.tiled = tiled_fns<F, NDIM, R>();
+        k.stream = stream_fns<F, NDIM, R>();
+    }
     k.march = march_fns<F, NDIM, R>();
     return k;
 }
@@ -355,6 +449,7 @@ static KernelSet select_set_r(int dyn, int n) {
     case ODP_DYN_DUBINS3D: return make_set<FDubins3D, 3, R>();
     case ODP_DYN_CAR4D: return make_set<FCar4D, 4, R>();
     case ODP_DYN_CAR5D: return make_set<FCar5D, 5, R>();
+    case ODP_DYN_PAIR_DUBINS3D: return make_set<FPairDubins3D, 3, R>();
     default: return make_set<FDoubleInt6D, 6, R>();
     }
 }
@@ -375,6 +470,7 @@ struct odp_grid {
     int64_t i0b = 0, n0 = 0;      // first owned axis-0 plane, owned planes
     nccl::comm_t comm = nullptr;
     float *d_range = nullptr;     // [-minD, maxD, maxabs, nan] of the current stage (allreduced)
+    float *d_amax = nullptr;      // per-CTA alpha^max of k_amax3 (DEPS3 functors)
     // device cache (allocated lazily on the device current at the first solve)
     int device = -1;
     float *d_tab = nullptr;
@@ -401,13 +497,13 @@ static void free_device(odp_grid *g) {
     cudaSetDevice(g->device);
     cudaFree(g->d_tab); cudaFree(g->d_dx);
     cudaFree(g->d_buf[0]); cudaFree(g->d_buf[1]);
-    cudaFree(g->d_partials); cudaFree(g->d_state); cudaFree(g->d_range);
+    cudaFree(g->d_partials); cudaFree(g->d_state); cudaFree(g->d_range); cudaFree(g->d_amax);
     if (g->h_state) cudaFreeHost(g->h_state);
     if (g->own_stream) cudaStreamDestroy(g->own_stream);
     for (auto e : g->events) cudaEventDestroy(e);
     g->events.clear();
     g->d_tab = nullptr; g->d_dx = nullptr; g->d_buf[0] = g->d_buf[1] = nullptr; g->d_partials = nullptr;
-    g->d_state = nullptr; g->h_state = nullptr; g->own_stream = nullptr; g->d_range = nullptr;
+    g->d_state = nullptr; g->h_state = nullptr; g->own_stream = nullptr; g->d_range = nullptr; g->d_amax = nullptr;
     g->max_parts = 0; g->buf_elems = 0;
     g->device = -1;
     if (cur >= 0) cudaSetDevice(cur);
@@ -565,6 +661,7 @@ static odp_status ensure_device(odp_grid *g, int nparts_needed) {
         g->max_parts = nparts_needed;
     }
     if (!g->d_range) CUDA_TRY(cudaMalloc(&g->d_range, (2 * MAXD + 2) * sizeof(float)));
+    if (!g->d_amax) CUDA_TRY(cudaMalloc(&g->d_amax, 1024 * MAXD * sizeof(float)));
     return ODP_OK;
 }
 
@@ -618,13 +715,13 @@ static odp_status range_allreduce(odp_grid *g, int n, cudaStream_t s) {
     return ODP_OK;
 }
 
-static const int kWantParams[6] = {2, 3, 3, 5, 3, 3};
-static const int kWantDims[6] = {0, 0, 3, 4, 5, 6};
+static const int kWantParams[7] = {2, 3, 3, 5, 3, 3, 5};
+static const int kWantDims[7] = {0, 0, 3, 4, 5, 6, 3};
 
 static odp_status validate(const odp_grid *g, int dyn, const double *params, int nparams, const double *tau,
                            int ntau, int accuracy, int mode) {
     if (!g) return fail(ODP_EINVAL, "NULL grid");
-    if (dyn < 0 || dyn > 5) return fail(ODP_EINVAL, "unknown dynamics id %d", dyn);
+    if (dyn < 0 || dyn > 6) return fail(ODP_EINVAL, "unknown dynamics id %d", dyn);
     if (!params || nparams != kWantParams[dyn]) return fail(ODP_EINVAL, "dynamics %d takes %d params (got %d)", dyn, kWantParams[dyn], nparams);
     if (kWantDims[dyn] && kWantDims[dyn] != g->n) return fail(ODP_EINVAL, "dynamics %d needs dims=%d (grid has %d)", dyn, kWantDims[dyn], g->n);
     const double goal = params[nparams - 1];
@@ -768,16 +865,20 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
     auto exch = [&](float *Wx) {
         if (g->nranks > 1 && cst == ODP_OK) cst = halo_exchange(g, Wx, R, s);
     };
+    const int namax = ks.amax3 ? nsm : 0;           // k_amax3 CTAs (DEPS3 functors)
     auto launch_fin = [&](int stage_in_step, int final_check) {
+        const float *rng = nullptr;
         if (g->comm) {
             ks.red<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, g->d_range);
             if (cst == ODP_OK) cst = range_allreduce(g, n, s);
-            ks.fin<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, gd, fp, g->d_dx, stage_in_step, final_check,
-                                     g->d_range);
-        } else {
-            ks.fin<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, gd, fp, g->d_dx, stage_in_step, final_check,
-                                     nullptr);
+            rng = g->d_range;
         }
+        if (ks.amax3 && stage_in_step == 0 && !final_check) {
+            ks.srange<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, rng);
+            ks.amax3<<<namax, 256, 0, s>>>(gd, fp, g->d_state, g->d_amax);
+        }
+        ks.fin<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, gd, fp, g->d_dx, stage_in_step, final_check,
+                                 rng, g->d_amax, namax);
     };
 
     // one timed/untimed launch wrapper; events are recorded only when kernel times are requested

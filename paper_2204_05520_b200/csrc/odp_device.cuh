@@ -115,7 +115,7 @@ __device__ __forceinline__ void fix_ghosts(float *v, int i, int N) {
 // ---------------------------------------------------------------------------------------------
 // Dynamics functors (reading A22).  Each provides
 //   NEED_X / NEED_TRIG  bitmasks of the axes whose coordinate / (cos, sin) the functor reads,
-//   deps(d)             bitmask of the axes alpha_d depends on (<= 2 axes),
+//   deps(d)             bitmask of the axes alpha_d depends on (<= 2 axes, or all 3 with DEPS3),
 //   init(P, minD, maxD) per-stage constants from params and the global derivative range,
 //   ham(pt, p)          H = p . f(x, u*, d*) with bang-bang u*, d* (Alg. 2 l.154-156, Eq. 4),
 //   alpha(d, pt)        max over p in [minD, maxD] of |dH/dp_d| (Alg. 2 l.162, reading A5).
@@ -137,6 +137,7 @@ template <int NDIM>
 struct FHoloBall {   // [ubar, goal]: xdot = u, |u|_2 <= ubar
     // alpha_(i,d) does not depend on the stage's derivative range: false
     static constexpr bool RANGE_FREE = false;
+    static constexpr bool SEPARABLE = true, DEPS3 = false;
     static constexpr int NEED_X = 0, NEED_TRIG = 0;
     static __host__ __device__ int deps(int) { return 0; }
     float kH, a[NDIM];
@@ -168,6 +169,7 @@ template <int NDIM>
 struct FHoloBox {    // [ubar, dbar, goal]: xdot_i = u_i + d_i
     // alpha_(i,d) does not depend on the stage's derivative range: true
     static constexpr bool RANGE_FREE = true;
+    static constexpr bool SEPARABLE = true, DEPS3 = false;
     static constexpr int NEED_X = 0, NEED_TRIG = 0;
     static __host__ __device__ int deps(int) { return 0; }
     float kH, a[NDIM];
@@ -192,6 +194,7 @@ struct FHoloBox {    // [ubar, dbar, goal]: xdot_i = u_i + d_i
 struct FDubins3D {   // [v, wbar, goal]: (x, y, th) -> (v cos th, v sin th, w)
     // alpha_(i,d) does not depend on the stage's derivative range: true
     static constexpr bool RANGE_FREE = true;
+    static constexpr bool SEPARABLE = true, DEPS3 = false;
     static constexpr int NDIM = 3;
     static constexpr int NEED_X = 0, NEED_TRIG = 1 << 2;
     static __host__ __device__ int deps(int d) { return d < 2 ? (1 << 2) : 0; }
@@ -213,6 +216,7 @@ struct FDubins3D {   // [v, wbar, goal]: (x, y, th) -> (v cos th, v sin th, w)
 struct FCar4D {      // [abar, wbar, dxbar, dybar, goal]: (x, y, v, th)
     // alpha_(i,d) does not depend on the stage's derivative range: false
     static constexpr bool RANGE_FREE = false;
+    static constexpr bool SEPARABLE = true, DEPS3 = false;
     static constexpr int NDIM = 4;
     static constexpr int NEED_X = 1 << 2, NEED_TRIG = 1 << 3;
     static __host__ __device__ int deps(int d) { return d < 2 ? ((1 << 2) | (1 << 3)) : 0; }
@@ -246,6 +250,7 @@ struct FCar4D {      // [abar, wbar, dxbar, dybar, goal]: (x, y, v, th)
 struct FCar5D {      // [abar, alphabar, goal]: (x, y, th, v, w)
     // alpha_(i,d) does not depend on the stage's derivative range: true
     static constexpr bool RANGE_FREE = true;
+    static constexpr bool SEPARABLE = true, DEPS3 = false;
     static constexpr int NDIM = 5;
     static constexpr int NEED_X = (1 << 3) | (1 << 4), NEED_TRIG = 1 << 2;
     static __host__ __device__ int deps(int d) {
@@ -277,6 +282,7 @@ struct FCar5D {      // [abar, alphabar, goal]: (x, y, th, v, w)
 struct FDoubleInt6D {  // [ubar, dbar, goal]: (px, vx, py, vy, pz, vz) -> (v_i, u_i + d_i)
     // alpha_(i,d) does not depend on the stage's derivative range: true
     static constexpr bool RANGE_FREE = true;
+    static constexpr bool SEPARABLE = true, DEPS3 = false;
     static constexpr int NDIM = 6;
     static constexpr int NEED_X = (1 << 1) | (1 << 3) | (1 << 5), NEED_TRIG = 0;
     static __host__ __device__ int deps(int d) { return (d & 1) == 0 ? (1 << (d + 1)) : 0; }
@@ -298,6 +304,56 @@ struct FDoubleInt6D {  // [ubar, dbar, goal]: (px, vx, py, vy, pz, vz) -> (v_i, 
     }
     __device__ float alpha(int d, const Pt &q) const {
         return (d & 1) == 0 ? fabsf(q.x[d + 1]) : av[d >> 1];
+    }
+};
+
+struct FPairDubins3D {  // Eq. 7 [va, vb, abar, bbar, goal]: relative (x, y, th) of a pursuer b
+                       // w.r.t. an evader a: xdot = -va + vb cos th + a y, ydot = va sin th - a x,
+                       // thdot = b - a; a (control) takes the goal's extremum, b the opposite (A30)
+    static constexpr int NDIM = 3;
+    static constexpr int NEED_X = (1 << 0) | (1 << 1), NEED_TRIG = 1 << 2;
+    // alpha_d depends on (x, y) through the switching function and on th through the drift
+    static __host__ __device__ int deps(int) { return 0x7; }
+    static constexpr bool RANGE_FREE = false;       // the sign set of q = p_x y - p_y x - p_th
+    static constexpr bool SEPARABLE = false, DEPS3 = true;
+    float va, vb, ka, kb;                            // ka = goal abar, kb = -goal bbar
+    float mn[3], mx[3];                              // the stage's costate box (A4)
+    __device__ void init(const FParams &P, const float *lo, const float *hi) {
+        va = P.c[0]; vb = P.c[1];
+        ka = P.c[4] * P.c[2];
+        kb = -P.c[4] * P.c[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) { mn[d] = lo[d]; mx[d] = hi[d]; }
+    }
+    __device__ float ham(const Pt &q, const float *p) const {
+        const float x = q.x[0], y = q.x[1];
+        const float sw = fmaf(p[0], y, -fmaf(p[1], x, p[2]));     // q = p_x y - p_y x - p_th
+        const float a = ka * sgn1(sw), b = kb * sgn1(p[2]);
+        float H = p[0] * fmaf(vb, q.c[2], fmaf(a, y, -va));
+        H = fmaf(p[1], fmaf(va, q.s[2], -a * x), H);
+        H = fmaf(p[2], b - a, H);
+        return H;
+    }
+    // alpha_{i,d}: maximum of |f_d| over the sign set of q on the costate box (exact: q is linear
+    // in p, its range is the sum of the ranges of its terms) and, for th, the sign set of p_th (A30)
+    __device__ float alpha(int d, const Pt &q) const {
+        const float x = q.x[0], y = q.x[1];
+        const float qlo = fminf(y * mn[0], y * mx[0]) + fminf(-x * mn[1], -x * mx[1]) - mx[2];
+        const float qhi = fmaxf(y * mn[0], y * mx[0]) + fmaxf(-x * mn[1], -x * mx[1]) - mn[2];
+        float best = 0.f;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const float sq = j == 0 ? 1.f : -1.f;
+            if (j == 0 ? !(qhi >= 0.f) : !(qlo < 0.f)) continue;
+            const float a = ka * sq;
+            if (d == 0) best = fmaxf(best, fabsf(fmaf(vb, q.c[2], fmaf(a, y, -va))));
+            else if (d == 1) best = fmaxf(best, fabsf(fmaf(va, q.s[2], -a * x)));
+            else {
+                if (mx[2] >= 0.f) best = fmaxf(best, fabsf(kb - a));
+                if (mn[2] < 0.f) best = fmaxf(best, fabsf(-kb - a));
+            }
+        }
+        return best;
     }
 };
 

@@ -108,6 +108,17 @@ def test_linear_field_dubins_drift_exact(acc):
     np.testing.assert_allclose(r.out[-1], X[0] + 0.3 * 0.8 * np.cos(X[2]), atol=1e-12)
 
 
+@pytest.mark.parametrize("acc", ["low", "medium"])
+def test_linear_field_pairwise_dubins_drift_exact(acc):
+    # Eq. 7 with abar = bbar = 0: f = (-va + vb cos th, va sin th, 0); V0 = x advances as
+    # V = x + t (-va + vb cos th) exactly (p = (1, 0, *), alpha_th = 0)
+    w = Workload("lin-pd", (9, 5, 12), (-4.0, -1.0, -math.pi), (4.0, 1.0, math.pi), (0, 0, 1), "PAIR_DUBINS3D",
+                 (0.8, 1.1, 0.0, 0.0, 1.0), (0.0, 0.3), acc, 0.8, "brs", ("plane", 0, 1.0, 0.0))
+    r = oracle.solve_workload(w)
+    X = _mesh(w)
+    np.testing.assert_allclose(r.out[-1], X[0] + 0.3 * (-0.8 + 1.1 * np.cos(X[2])), atol=1e-12)
+
+
 def test_linear_solve_spec_example():
     # 1D, f = 1, phi0 = x on [-2, 2], horizon 0.5 -> x + 0.5 within 1e-9 (max with u in [-1,1])
     w = Workload("lin1d", (41,), (-2.0,), (2.0,), (0,), "HOLONOMIC_BOX", (1.0, 0.0, 1.0), (0.0, 0.5), "low", 0.8,
@@ -202,6 +213,8 @@ TINY = [
     ("CAR4D", (1.5, 1.0, 0.25, 0.25, -1.0), 4, (3,)),
     ("CAR5D", (1.0, 2.0, -1.0), 5, (2,)),
     ("DOUBLEINT6D", (1.0, 0.2, -1.0), 6, ()),
+    ("PAIR_DUBINS3D", (1.0, 1.2, 1.0, 0.8, 1.0), 3, (2,)),
+    ("PAIR_DUBINS3D", (0.8, 1.0, 0.5, 0.7, -1.0), 3, (2,)),
 ]
 
 

@@ -146,7 +146,10 @@ FUNCTORS = [
     ("CAR5D", (1.0, 2.0, -1.0), 5, None),
     ("DOUBLEINT6D", (1.0, 0.2, -1.0), 6, None),
     ("DOUBLEINT6D", (1.0, 0.2, 1.0), 6, None),
+    ("PAIR_DUBINS3D", (5.0, 5.0, 1.0, 1.0, 1.0), 3, None),     # Eq. 7, air3D-like speeds
+    ("PAIR_DUBINS3D", (1.0, 1.5, 0.7, 0.4, -1.0), 3, None),
 ]
+ALPHA_FUNCTORS = [f for f in FUNCTORS if f[0] != "PAIR_DUBINS3D"]
 
 
 @pytest.mark.parametrize("dyn,prm,n,_", FUNCTORS)
@@ -199,7 +202,7 @@ def test_ball_hamiltonian_closed_form():
 
 
 # ---- a5/a7: alpha (Alg. 2 l.162; reading A5) ------------------------------------------------------
-@pytest.mark.parametrize("dyn,prm,n,_", FUNCTORS)
+@pytest.mark.parametrize("dyn,prm,n,_", ALPHA_FUNCTORS)
 def test_alpha_dominates_and_is_attained(dyn, prm, n, _):
     rng = np.random.default_rng(5)
     for trial in range(60):
@@ -251,3 +254,35 @@ def test_alpha_config_values_table_c2():
     w = CONFIGS["c4"]
     al = oracle.alpha("DOUBLEINT6D", w.params, [0, 2.0, 0, -2.0, 0, 1.0], [-1] * 6, [1] * 6)
     np.testing.assert_allclose(al, [2.0, 0.8, 2.0, 0.8, 1.0, 0.8], atol=1e-12)
+
+
+@pytest.mark.parametrize("prm", [(5.0, 5.0, 1.0, 1.0, 1.0), (1.0, 1.5, 0.7, 0.4, -1.0)])
+def test_alpha_pairwise_dubins_eq7(prm):
+    # A30: alpha over the sign set of q = p_x y - p_y x - p_th (exact range over the box, linear in p)
+    # and, for th, the sign set of p_th taken independently.  x, y: exact maximum (attained at a box
+    # corner); th: an upper bound of |dH/dp_th| (dominance), equal to abar + bbar when q and p_th
+    # can take both signs.
+    rng = np.random.default_rng(17)
+    for trial in range(80):
+        x = rng.uniform(-6, 6, 3)
+        a, b = rng.normal(size=3), rng.normal(size=3)
+        if trial % 3 == 0:
+            b = a + np.abs(rng.normal(size=3))
+        minD, maxD = np.minimum(a, b), np.maximum(a, b)
+        al = oracle.alpha("PAIR_DUBINS3D", prm, x, minD, maxD)
+        Ab = brute.alpha("PAIR_DUBINS3D", prm, [np.array(v) for v in x], minD, maxD)
+        np.testing.assert_allclose(al, [float(v) for v in Ab], atol=1e-12)
+        best = np.zeros(3)
+        for _ in range(300):
+            p = rng.uniform(minD, maxD)
+            _, _, _, f = oracle.hamiltonian("PAIR_DUBINS3D", prm, x, p)
+            assert np.all(np.abs(f) <= al + 1e-12)
+            best = np.maximum(best, np.abs(f))
+        for corner in range(8):
+            p = np.where([(corner >> k) & 1 for k in range(3)], maxD, minD)
+            _, _, _, f = oracle.hamiltonian("PAIR_DUBINS3D", prm, x, p)
+            best = np.maximum(best, np.abs(f))
+        np.testing.assert_allclose(best[:2], al[:2], atol=1e-12)
+    # both sign sets full -> alpha_th = abar + bbar
+    al = oracle.alpha("PAIR_DUBINS3D", prm, [1.0, 2.0, 0.3], [-1.0, -1.0, -1.0], [1.0, 1.0, 1.0])
+    assert al[2] == pytest.approx(prm[2] + prm[3], rel=1e-15)
