@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -901,6 +902,75 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
 
     int cur = 0;                       // index of the buffer holding the current V
     odp_status rs = ODP_OK;
+    // one time step (Alg. 2 l.150-170) as a launch sequence; a = buffer of the current V (LOW)
+    auto step = [&](int a, bool sp_mode) -> odp_status {
+        const int b = a ^ 1;
+        odp_status r = ODP_OK;
+        if (sp_mode) {
+            // pass 2 only: dt from the fixed alpha^max, the guard on each stage's output
+            if ((r = rec(2, [&] { k_dt<<<1, 1, 0, s>>>(g->d_state, g->d_dx, n); }))) return r;
+            if (accuracy == ODP_LOW) {
+                if (g->nranks > 1 && (r = rec(2, [&] { exch(buf[a]); }))) return r;
+                if ((r = rec(1, [&] { launch_pass2(buf[a], nullptr, buf[b], STAGE_EULER, true); }))) return r;
+                if ((r = rec(2, [&] { launch_guard(1); }))) return r;
+            } else {
+                if (g->nranks > 1 && (r = rec(2, [&] { exch(buf[0]); }))) return r;
+                if ((r = rec(1, [&] { launch_pass2(buf[0], nullptr, buf[1], STAGE_RK1, true); }))) return r;
+                if ((r = rec(2, [&] { launch_guard(0); }))) return r;
+                if (g->nranks > 1 && (r = rec(2, [&] { exch(buf[1]); }))) return r;
+                if ((r = rec(1, [&] { launch_pass2(buf[1], buf[0], buf[0], STAGE_RK2, true); }))) return r;
+                if ((r = rec(2, [&] { launch_guard(1); }))) return r;
+            }
+        } else if (accuracy == ODP_LOW) {
+            if (g->nranks > 1 && (r = rec(2, [&] { exch(buf[a]); }))) return r;
+            if ((r = rec(0, [&] { launch_pass1(buf[a]); }))) return r;
+            if ((r = rec(2, [&] { launch_fin(0, 0); }))) return r;
+            if ((r = rec(1, [&] { launch_pass2(buf[a], nullptr, buf[b], STAGE_EULER); }))) return r;
+        } else {
+            if (g->nranks > 1 && (r = rec(2, [&] { exch(buf[0]); }))) return r;
+            if ((r = rec(0, [&] { launch_pass1(buf[0]); }))) return r;
+            if ((r = rec(2, [&] { launch_fin(0, 0); }))) return r;
+            if ((r = rec(1, [&] { launch_pass2(buf[0], nullptr, buf[1], STAGE_RK1); }))) return r;
+            if (g->nranks > 1 && (r = rec(2, [&] { exch(buf[1]); }))) return r;
+            if ((r = rec(0, [&] { launch_pass1(buf[1]); }))) return r;
+            if ((r = rec(2, [&] { launch_fin(1, 0); }))) return r;
+            if ((r = rec(1, [&] { launch_pass2(buf[1], buf[0], buf[0], STAGE_RK2); }))) return r;
+        }
+        return rec(2, [&] { k_advance<<<1, 1, 0, s>>>(g->d_state); });
+    };
+    // CUDA graphs (opts.use_graph: 0 auto = grids up to 2^25 local points, 1 on, -1 off): GS steps
+    // captured once per (step kind, buffer parity) and replayed as one launch; every kernel
+    // early-exits once the interval is done, exactly like the direct launches.  Not with kernel
+    // timing (per-launch events) or an NCCL communicator.
+    constexpr int GS = 8;
+    const int ug = opts ? opts->use_graph : 0;
+    const bool graphs = !timed && !g->comm && (ug == 1 || (ug == 0 && local_points(g) <= (1LL << 25)));
+    cudaGraphExec_t gexec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    long long glaunch[2] = {0, 0};          // kernel launches per replay, by step kind
+    auto graph_of = [&](int kind_sp, int a0, cudaGraphExec_t *out_exec) -> odp_status {
+        if (gexec[kind_sp][a0]) { *out_exec = gexec[kind_sp][a0]; return ODP_OK; }
+        const long long l0 = g->launches;
+        cudaGraph_t graph = nullptr;
+        CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        odp_status r = ODP_OK;
+        for (int j = 0; j < GS && r == ODP_OK; ++j) r = step((a0 + j) & 1, kind_sp != 0);
+        const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+        if (r) { if (graph) cudaGraphDestroy(graph); return r; }
+        if (ce != cudaSuccess) return fail(ODP_ECUDA, "graph capture: %s", cudaGetErrorString(ce));
+        const cudaError_t ie = cudaGraphInstantiate(&gexec[kind_sp][a0], graph, 0);
+        cudaGraphDestroy(graph);
+        if (ie != cudaSuccess) return fail(ODP_ECUDA, "graph instantiate: %s", cudaGetErrorString(ie));
+        glaunch[kind_sp] = g->launches - l0;
+        g->launches = l0;
+        *out_exec = gexec[kind_sp][a0];
+        return ODP_OK;
+    };
+    auto free_graphs = [&]() {
+        for (auto &row : gexec)
+            for (auto &e : row)
+                if (e) { cudaGraphExecDestroy(e); e = nullptr; }
+    };
+    struct GraphGuard { std::function<void()> f; ~GraphGuard() { f(); } } graph_guard{free_graphs};
     for (int k = 1; k < ntau && rs == ODP_OK; ++k) {
         k_begin<<<1, 1, 0, s>>>(g->d_state, tau[k]);
         ++g->launches;
@@ -913,41 +983,20 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
             launches.clear();
             step_of_launch.clear();
             ev_next = 0;
-            for (int j = 0; j < chunk; ++j) {
-                const int a = (cur + j) & 1, b = a ^ 1;
-                if (single && have_amax) {
-                    // pass 2 only: dt from the fixed alpha^max, the guard on each stage's output
-                    if ((rs = rec(2, [&] { k_dt<<<1, 1, 0, s>>>(g->d_state, g->d_dx, n); }))) return rs;
-                    if (accuracy == ODP_LOW) {
-                        if (g->nranks > 1 && (rs = rec(2, [&] { exch(buf[a]); }))) return rs;
-                        if ((rs = rec(1, [&] { launch_pass2(buf[a], nullptr, buf[b], STAGE_EULER, true); }))) return rs;
-                        if ((rs = rec(2, [&] { launch_guard(1); }))) return rs;
-                    } else {
-                        if (g->nranks > 1 && (rs = rec(2, [&] { exch(buf[0]); }))) return rs;
-                        if ((rs = rec(1, [&] { launch_pass2(buf[0], nullptr, buf[1], STAGE_RK1, true); }))) return rs;
-                        if ((rs = rec(2, [&] { launch_guard(0); }))) return rs;
-                        if (g->nranks > 1 && (rs = rec(2, [&] { exch(buf[1]); }))) return rs;
-                        if ((rs = rec(1, [&] { launch_pass2(buf[1], buf[0], buf[0], STAGE_RK2, true); }))) return rs;
-                        if ((rs = rec(2, [&] { launch_guard(1); }))) return rs;
-                    }
-                } else if (accuracy == ODP_LOW) {
-                    if (g->nranks > 1 && (rs = rec(2, [&] { exch(buf[a]); }))) return rs;
-                    if ((rs = rec(0, [&] { launch_pass1(buf[a]); }))) return rs;
-                    if ((rs = rec(2, [&] { launch_fin(0, 0); }))) return rs;
-                    if ((rs = rec(1, [&] { launch_pass2(buf[a], nullptr, buf[b], STAGE_EULER); }))) return rs;
-                } else {
-                    if (g->nranks > 1 && (rs = rec(2, [&] { exch(buf[0]); }))) return rs;
-                    if ((rs = rec(0, [&] { launch_pass1(buf[0]); }))) return rs;
-                    if ((rs = rec(2, [&] { launch_fin(0, 0); }))) return rs;
-                    if ((rs = rec(1, [&] { launch_pass2(buf[0], nullptr, buf[1], STAGE_RK1); }))) return rs;
-                    if (g->nranks > 1 && (rs = rec(2, [&] { exch(buf[1]); }))) return rs;
-                    if ((rs = rec(0, [&] { launch_pass1(buf[1]); }))) return rs;
-                    if ((rs = rec(2, [&] { launch_fin(1, 0); }))) return rs;
-                    if ((rs = rec(1, [&] { launch_pass2(buf[1], buf[0], buf[0], STAGE_RK2); }))) return rs;
+            const bool sp_now = single && have_amax;
+            if (graphs && chunk >= GS && (!single || have_amax)) {
+                cudaGraphExec_t ex = nullptr;
+                if ((rs = graph_of(sp_now ? 1 : 0, cur & 1, &ex))) return rs;
+                for (int r = 0; r < (chunk + GS - 1) / GS; ++r) {
+                    CUDA_TRY(cudaGraphLaunch(ex, s));
+                    g->launches += glaunch[sp_now ? 1 : 0];
                 }
-                if ((rs = rec(2, [&] { k_advance<<<1, 1, 0, s>>>(g->d_state); }))) return rs;
-                have_amax = true;
-                while (step_of_launch.size() < launches.size()) step_of_launch.push_back(j);
+            } else {
+                for (int j = 0; j < chunk; ++j) {
+                    if ((rs = step((cur + j) & 1, single && have_amax))) return rs;
+                    have_amax = true;
+                    while (step_of_launch.size() < launches.size()) step_of_launch.push_back(j);
+                }
             }
             CUDA_TRY(cudaGetLastError());
             if (cst) return cst;
