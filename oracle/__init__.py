@@ -62,6 +62,8 @@ def lib():
         _lib.oracle_hj_solve.argtypes = [c_int, I64, D, D, c_u32, c_int, D, c_int, F, F, D, c_int, c_int,
                                          c_int, c_dbl, c_int, c_int, D, D, D, I64, I64, c_int,
                                          ctypes.c_void_p]
+        _lib.oracle_ttr_solve.argtypes = [c_int, I64, D, D, c_u32, c_int, D, c_int, F, c_dbl, c_dbl,
+                                          ctypes.c_int64, D, I64, D]
         _lib.oracle_max_threads.restype = c_int
         _lib.oracle_cfl_dt.argtypes = [c_int, D, D, c_dbl, c_dbl]
         _lib.oracle_cfl_dt.restype = c_dbl
@@ -236,6 +238,29 @@ def hj_solve(N, lo, hi, periodic_mask: int, dyn: str, params, V0, tau: Sequence[
     r = SolveResult(out, tr.value, steps.value, stages.value, st)
     r.ambiguous = amb
     return r
+
+
+def ttr_solve(N, lo, hi, periodic_mask: int, dyn: str, params, V0, eps: float = 1e-6, max_sweeps: int = 10000,
+              big: float = 100.0):
+    """Time-to-reach by Lax-Friedrichs sweeping (Alg. 3, readings A31-A34).  Target = {V0 <= 0}.
+    Returns (phi float64 array of shape N, sweeps, last max |phi - phi_old|)."""
+    N = tuple(int(v) for v in N)
+    n = len(N)
+    V0 = np.ascontiguousarray(V0, dtype=np.float32).reshape(N)
+    Na, Np = _i64(N)
+    loa, lop = _d(lo)
+    hia, hip = _d(hi)
+    pa, pp = _d(params)
+    out = np.zeros(N, dtype=np.float64)
+    sw = ctypes.c_int64()
+    ch = ctypes.c_double()
+    st = lib().oracle_ttr_solve(n, Np, lop, hip, periodic_mask, DYN_IDS[dyn], pp, len(pa),
+                                V0.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), float(big), float(eps),
+                                int(max_sweeps), out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                ctypes.byref(sw), ctypes.byref(ch))
+    if st:
+        raise OracleError(st)
+    return out, sw.value, ch.value
 
 
 def solve_workload(w, V0=None, seed=None, **kw) -> SolveResult:

@@ -247,3 +247,72 @@ def solve(w, V0, cfl=None, store_initial=False):
             steps += 1
         outs.append(V.copy())
     return np.stack(outs), steps
+
+
+
+def _ttr_setup(N, lo, hi, periodic, dyn, params):
+    n = len(N)
+    prm = list(params)
+    prm[-1] = -1.0
+    dx = [(hi[d] - lo[d]) / (N[d] if periodic[d] else N[d] - 1) for d in range(n)]
+    axes = [lo[d] + np.arange(N[d]) * dx[d] for d in range(n)]
+    X = np.meshgrid(*axes, indexing="ij")
+    sig = [np.broadcast_to(s, tuple(N)) for s in alpha(dyn, prm, X, [-1.0] * n, [1.0] * n)]
+    interior = np.ones(tuple(N), dtype=bool)
+    for d in range(n):
+        if not periodic[d]:
+            sl = [slice(None)] * n
+            sl[d] = 0
+            interior[tuple(sl)] = False
+            sl[d] = N[d] - 1
+            interior[tuple(sl)] = False
+    return n, prm, dx, X, sig, interior
+
+
+def ttr_update_map(N, lo, hi, periodic, dyn, params, phi):
+    """The Lax-Friedrichs update of Alg. 3 l.5-11 (readings A32-A33) evaluated at every node from
+    the iterate phi, H by vertex enumeration (hamiltonian() with goal -1), sigma from alpha() on
+    the box [-1, 1]^n.  Values on non-periodic faces are meaningless (rolls wrap there)."""
+    n, prm, dx, X, sig, _ = _ttr_setup(N, lo, hi, periodic, dyn, params)
+    P, num = [], 0.0
+    for d in range(n):
+        vp, vm = np.roll(phi, -1, axis=d), np.roll(phi, 1, axis=d)
+        P.append((vp - vm) / (2 * dx[d]))
+        num = num + sig[d] * (vp + vm) / (2 * dx[d])
+    den = sum(sig[d] / dx[d] for d in range(n))
+    H = -hamiltonian(dyn, prm, X, P) - 1.0
+    return np.where(den > 0, (num - H) / np.where(den > 0, den, 1.0), phi)
+
+
+def ttr_boundary_rule(N, periodic, phi):
+    """Alg. 3 l.14-15 along each non-periodic axis in order (reading A34), in place."""
+    n = len(N)
+    for d in range(n):
+        if periodic[d]:
+            continue
+
+        def sl(i):
+            s = [slice(None)] * n
+            s[d] = i
+            return tuple(s)
+        for e, a, b in ((0, 1, 2), (N[d] - 1, N[d] - 2, N[d] - 3)):
+            phi[sl(e)] = np.minimum(np.maximum(2 * phi[sl(a)] - phi[sl(b)], phi[sl(b)]), phi[sl(e)])
+    return phi
+
+
+def ttr_jacobi(N, lo, hi, periodic, dyn, params, V0, eps=1e-12, max_iter=200000, big=100.0):
+    """Independent NumPy formulation of the time-to-reach iteration (Alg. 3, readings A31-A34):
+    Jacobi iterations (all nodes from the previous iterate) of ttr_update_map, then the boundary
+    rule.  Its fixed point equals the oracle's Gauss-Seidel one where the boundary rule's min
+    never binds on a non-monotone path (holonomic cases); see test_oracle_ttr."""
+    _, _, _, _, _, interior = _ttr_setup(N, lo, hi, periodic, dyn, params)
+    target = np.asarray(V0, dtype=np.float32) <= 0
+    phi = np.where(target, 0.0, big)
+    upd = interior & ~target
+    for it in range(max_iter):
+        old = phi.copy()
+        phi = np.where(upd, np.minimum(ttr_update_map(N, lo, hi, periodic, dyn, params, phi), phi), phi)
+        ttr_boundary_rule(N, periodic, phi)
+        if np.abs(phi - old).max() <= eps:
+            return phi, it + 1
+    return phi, max_iter

@@ -649,6 +649,99 @@ double oracle_cfl_dt(int n, const double *amax, const double *dx, double cfl, do
     return og_dt(n, amax, dx, cfl, remaining);
 }
 
+/* ------------------------------------------------------------------------------------------
+ * Time-to-reach by Lax-Friedrichs sweeping -- Algorithm 3 with Eq. 5-6
+ * and the alternating sweep orderings of §4.3.  Readings:
+ *   A31 the loop runs WHILE max |phi - phi_old| > eps (the printed "<" would never enter it);
+ *       l.3 "phi <- phi_old" saves the previous iterate.
+ *   A32 H_TTR(z, p) = max_u min_d (-p.f) - 1 (Eq. 6, min/max swapped by the Isaacs condition of
+ *       these control-affine systems) = -H_reach(z, p) - 1, H_reach the Hamiltonian of the functor
+ *       with goal -1 (the control minimises p.f); p by central differences (the LF form of l.11).
+ *   A33 sigma_d(z) = max over all costates of |dH/dp_d| (the functor's alpha with every costate
+ *       sign possible, i.e. on the box [-1, 1]^n); in n dimensions l.10-11 read
+ *       phi_new = (-H + sum_d sigma_d (phi_{+d} + phi_{-d}) / (2 dz_d)) / (sum_d sigma_d / dz_d).
+ *   A34 target nodes (V0 <= 0) keep phi = 0; "not in boundary" = index 1..N-2 on every
+ *       non-periodic axis; after each sweep the boundary rule of l.14-15 is applied along each
+ *       non-periodic axis in order 0..n-1 to that axis' face nodes.
+ *   Sweep k orders axis d descending when bit (d mod n) of k is set (2^n orderings, Gauss-Seidel).
+ * ---------------------------------------------------------------------------------------- */
+static double ttr_update(const og *g, const ofun *fr, const double *phi, const int64_t *idx, int64_t flat,
+                         const double *x) {
+    double p[6] = {0}, sig[6] = {0}, mn[6], mx[6];
+    for (int d = 0; d < g->n; ++d) { mn[d] = -1.0; mx[d] = 1.0; }
+    double num = 0.0, den = 0.0;
+    for (int d = 0; d < g->n; ++d) {
+        const int64_t base = flat - idx[d] * g->stride[d];
+        const double vp = og_at(g, phi, base, d, idx[d] + 1), vm = og_at(g, phi, base, d, idx[d] - 1);
+        p[d] = (vp - vm) / (2.0 * g->dx[d]);
+        sig[d] = of_alpha(fr, x, d, mn, mx);
+        num += sig[d] * (vp + vm) / (2.0 * g->dx[d]);
+        den += sig[d] / g->dx[d];
+    }
+    const double H = -of_ham(fr, x, p) - 1.0;                       /* A32 */
+    return den > 0.0 ? (num - H) / den : phi[flat];
+}
+
+int oracle_ttr_solve(int n, const int64_t *N, const double *lo, const double *hi, uint32_t pmask, int dyn,
+                     const double *prm, int np, const float *V0, double big, double eps, int64_t max_sweeps,
+                     double *out, int64_t *sweeps_out, double *last_change) {
+    og g;
+    ofun f;
+    int st = og_init(&g, n, N, lo, hi, pmask);
+    if (st) { og_free(&g); return st; }
+    /* the control minimises p.f (goal -1) whatever the caller's goal says (A32) */
+    double prm2[8];
+    for (int k = 0; k < np && k < 8; ++k) prm2[k] = prm[k];
+    if (np >= 1) prm2[np - 1] = -1.0;
+    if ((st = of_init(&f, dyn, n, prm2, np))) { og_free(&g); return st; }
+    if (!(eps > 0.0) || max_sweeps < 1) { og_free(&g); return OR_EINVAL; }
+    const int64_t P = g.P;
+    double *old = (double *)malloc(sizeof(double) * (size_t)P);
+    if (!old) { og_free(&g); return OR_ENOMEM; }
+    for (int64_t i = 0; i < P; ++i) out[i] = V0[i] <= 0.0f ? 0.0 : big;     /* l.1 */
+    int64_t sweeps = 0;
+    double change = INFINITY;
+    while (change > eps && sweeps < max_sweeps) {                            /* l.2, A31 */
+        memcpy(old, out, sizeof(double) * (size_t)P);                        /* l.3 */
+        for (int64_t k = 0; k < P; ++k) {                                    /* l.4: one ordering */
+            int64_t idx[6], r = k, flat = 0;
+            int skip = 0;
+            for (int d = n - 1; d >= 0; --d) {
+                int64_t i = r % g.N[d];
+                r /= g.N[d];
+                if ((sweeps >> (d % 30)) & 1) i = g.N[d] - 1 - i;
+                idx[d] = i;
+                if (!g.per[d] && (i == 0 || i == g.N[d] - 1)) skip = 1;
+            }
+            if (skip) continue;
+            for (int d = 0; d < n; ++d) flat += idx[d] * g.stride[d];
+            if (V0[flat] <= 0.0f) continue;                                   /* A34 */
+            double x[6];
+            for (int d = 0; d < n; ++d) x[d] = g.x[d][idx[d]];
+            const double nv = ttr_update(&g, &f, out, idx, flat, x);         /* l.5-11 */
+            out[flat] = fmin(nv, out[flat]);                                  /* l.12 */
+        }
+        for (int d = 0; d < n; ++d) {                                         /* l.14-15 */
+            if (g.per[d]) continue;
+            const int64_t s = g.stride[d], Nd = g.N[d];
+            for (int64_t k = 0; k < P; ++k) {
+                const int64_t i = (k / s) % Nd;
+                if (i != 0 && i != Nd - 1) continue;
+                const int64_t a = i == 0 ? k + s : k - s, b = i == 0 ? k + 2 * s : k - 2 * s;
+                out[k] = fmin(fmax(2.0 * out[a] - out[b], out[b]), out[k]);
+            }
+        }
+        change = 0.0;
+        for (int64_t i = 0; i < P; ++i) change = fmax(change, fabs(out[i] - old[i]));
+        ++sweeps;
+    }
+    free(old);
+    og_free(&g);
+    if (sweeps_out) *sweeps_out = sweeps;
+    if (last_change) *last_change = change;
+    return OR_OK;
+}
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();
