@@ -172,6 +172,44 @@ odp_status odp_comm_unique_id(void *id128);
 odp_status odp_grid_partition(odp_grid *g, int rank, int nranks, const void *id128, int device);
 odp_status odp_grid_local_extent(const odp_grid *g, int64_t *i0_begin, int64_t *i0_count);
 
+/*
+ * Time-to-reach: the stationary HJ equation of Eq. 6 for the TTR
+ * function phi(z) = min time to reach the target T = {V0 <= 0} (Eq. 5), by the
+ * Lax-Friedrichs iteration of Algorithm 3: phi = 0 on T and `big` elsewhere (l.1);
+ * every node not on a non-periodic face takes
+ *     phi_new = min(phi, (-H + sum_d sigma_d (phi_{+d} + phi_{-d}) / (2 dz_d)) / (sum_d sigma_d / dz_d))
+ * with p = central differences, H = -H_reach(z, p) - 1 (the functor's Hamiltonian with goal -1,
+ * whatever params[last] says; it must still be -1 or +1) and sigma_d the functor's alpha on the
+ * costate box [-1, 1]^n (readings A32, A33); then along each non-periodic axis in order the faces
+ * take min(max(2 phi_1 - phi_2, phi_2), phi_face) (l.14-15, A34); repeat while
+ * max |phi - phi_old| > eps (A31).  The GPU iterates in Jacobi order (A35): every node of
+ * iteration k+1 from iteration k -- Algorithm 3's fixed point without its sequential dependence.
+ *
+ *   V0   DEVICE pointer, points() floats: the target is {V0 <= 0}
+ *   phi  DEVICE pointer, points() floats: the result (float32).  Must not alias V0.
+ *   opts nullable.
+ * Errors: ODP_EINVAL (bad dynamics/params as odp_hj_solve, a non-periodic axis with N < 4, a
+ * partitioned handle, NULL pointers); ODP_ECUDA; ODP_ENOMEM.  Returns after the device work.
+ * Iterations stop at max_iters even if the change is still above eps (iters_taken says so).
+ */
+typedef struct {
+    double eps;               /* stop once max |phi - phi_old| <= eps; <= 0 -> 1e-6 (A31)        */
+    long long max_iters;      /* <= 0 -> 100000                                                  */
+    double big;               /* initial value off the target; <= 0 -> 100 (l.1)                 */
+    void *stream;             /* cudaStream_t; NULL -> the library's own stream                  */
+    int use_graph;            /* 1 -> replay chunks of iterations as a CUDA graph                */
+    long long *iters_taken;   /* optional out: iterations executed                               */
+    double *last_change;      /* optional out: max |phi - phi_old| of the last iteration         */
+    double *kernel_ms;        /* optional out: device time of the iteration loop                 */
+} odp_ttr_opts;
+
+odp_status odp_ttr_solve(odp_grid *g, int dynamics_id, const double *params, int nparams,
+                         const float *V0, float *phi, const odp_ttr_opts *opts);
+
+/* As odp_ttr_solve with HOST V0 and phi (copies inside the call). */
+odp_status odp_ttr_solve_host(odp_grid *g, int dynamics_id, const double *params, int nparams,
+                              const float *V0, float *phi, const odp_ttr_opts *opts);
+
 /* Number of kernel launches issued by the last solve on this handle (launch accounting). */
 long long odp_last_launch_count(const odp_grid *g);
 

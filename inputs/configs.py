@@ -106,6 +106,17 @@ F2 = Workload(
 CONFIGS = {w.name: w for w in (C1, C2, C3, C4, C5_LOW, C5_MED, F2)}
 
 
+# time-to-reach (Algorithm 3) workloads.  The paper benchmarks no TTR
+# problem, so the bench case is the classic Dubins-car TTR to a disc (reading A35): v = 1, |w| <= 1,
+# x, y in [-5, 5], th in [-pi, pi) periodic, target disc of radius 1 at the origin, 256^3 nodes
+# (3 float32 arrays = 200 MB, above L2).  tau / accuracy / cfl / mode are unused by the TTR path.
+T1 = Workload(
+    name="t1", N=(256, 256, 256), lo=(-5.0, -5.0, -PI), hi=(5.0, 5.0, PI), periodic=(0, 0, 1),
+    dynamics="DUBINS3D", params=(1.0, 1.0, -1.0), tau=(0.0, 1.0), accuracy="low", cfl=0.8, mode="brt",
+    target=("cylinder", (0, 1), 1.0), note="Dubins-car time-to-reach a unit disc, 256^3")
+TTR_CONFIGS = {T1.name: T1}
+
+
 def axis_nodes(N: int, lo: float, hi: float, periodic: bool) -> np.ndarray:
     """Node positions of one axis (problem statement; reading A15)."""
     h = (hi - lo) / (N if periodic else (N - 1))

@@ -269,11 +269,11 @@ def _ttr_setup(N, lo, hi, periodic, dyn, params):
     return n, prm, dx, X, sig, interior
 
 
-def ttr_update_map(N, lo, hi, periodic, dyn, params, phi):
+def ttr_update_map(N, lo, hi, periodic, dyn, params, phi, setup=None):
     """The Lax-Friedrichs update of Alg. 3 l.5-11 (readings A32-A33) evaluated at every node from
     the iterate phi, H by vertex enumeration (hamiltonian() with goal -1), sigma from alpha() on
     the box [-1, 1]^n.  Values on non-periodic faces are meaningless (rolls wrap there)."""
-    n, prm, dx, X, sig, _ = _ttr_setup(N, lo, hi, periodic, dyn, params)
+    n, prm, dx, X, sig, _ = setup or _ttr_setup(N, lo, hi, periodic, dyn, params)
     P, num = [], 0.0
     for d in range(n):
         vp, vm = np.roll(phi, -1, axis=d), np.roll(phi, 1, axis=d)
@@ -305,13 +305,14 @@ def ttr_jacobi(N, lo, hi, periodic, dyn, params, V0, eps=1e-12, max_iter=200000,
     Jacobi iterations (all nodes from the previous iterate) of ttr_update_map, then the boundary
     rule.  Its fixed point equals the oracle's Gauss-Seidel one where the boundary rule's min
     never binds on a non-monotone path (holonomic cases); see test_oracle_ttr."""
-    _, _, _, _, _, interior = _ttr_setup(N, lo, hi, periodic, dyn, params)
+    setup = _ttr_setup(N, lo, hi, periodic, dyn, params)
+    interior = setup[5]
     target = np.asarray(V0, dtype=np.float32) <= 0
     phi = np.where(target, 0.0, big)
     upd = interior & ~target
     for it in range(max_iter):
         old = phi.copy()
-        phi = np.where(upd, np.minimum(ttr_update_map(N, lo, hi, periodic, dyn, params, phi), phi), phi)
+        phi = np.where(upd, np.minimum(ttr_update_map(N, lo, hi, periodic, dyn, params, phi, setup), phi), phi)
         ttr_boundary_rule(N, periodic, phi)
         if np.abs(phi - old).max() <= eps:
             return phi, it + 1

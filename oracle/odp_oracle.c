@@ -663,7 +663,9 @@ double oracle_cfl_dt(int n, const double *amax, const double *dx, double cfl, do
  *   A34 target nodes (V0 <= 0) keep phi = 0; "not in boundary" = index 1..N-2 on every
  *       non-periodic axis; after each sweep the boundary rule of l.14-15 is applied along each
  *       non-periodic axis in order 0..n-1 to that axis' face nodes.
- *   Sweep k orders axis d descending when bit (d mod n) of k is set (2^n orderings, Gauss-Seidel).
+ *   A35 (oracle side) sweep k visits axis d < 3 descending when bit d of (k mod 8) is set, axes >= 3
+ *       ascending: the 8 alternating orderings of §4.3 ("a total of 8 different iterating
+ *       directions"); Gauss-Seidel, in place, as Algorithm 3 prints.
  * ---------------------------------------------------------------------------------------- */
 static double ttr_update(const og *g, const ofun *fr, const double *phi, const int64_t *idx, int64_t flat,
                          const double *x) {
@@ -709,7 +711,7 @@ int oracle_ttr_solve(int n, const int64_t *N, const double *lo, const double *hi
             for (int d = n - 1; d >= 0; --d) {
                 int64_t i = r % g.N[d];
                 r /= g.N[d];
-                if ((sweeps >> (d % 30)) & 1) i = g.N[d] - 1 - i;
+                if (d < 3 && (((sweeps & 7) >> d) & 1)) i = g.N[d] - 1 - i;       /* A35 */
                 idx[d] = i;
                 if (!g.per[d] && (i == 0 || i == g.N[d] - 1)) skip = 1;
             }

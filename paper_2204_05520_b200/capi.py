@@ -24,7 +24,7 @@ DYNAMICS = {"HOLONOMIC_BALL": 0, "HOLONOMIC_BOX": 1, "DUBINS3D": 2, "CAR4D": 3, 
 # every symbol include/odp.h declares (checked by tests/test_capi_host.py)
 EXPORTS = ("odp_grid_create", "odp_grid_destroy", "odp_grid_info", "odp_hj_solve", "odp_hj_solve_host",
            "odp_partition_extent", "odp_comm_unique_id", "odp_grid_partition", "odp_grid_local_extent",
-           "odp_last_launch_count", "odp_last_error", "odp_version")
+           "odp_last_launch_count", "odp_last_error", "odp_version", "odp_ttr_solve", "odp_ttr_solve_host")
 
 
 class odp_solve_opts(ctypes.Structure):
@@ -40,6 +40,17 @@ class odp_solve_opts(ctypes.Structure):
                 ("kernel_ms", ctypes.POINTER(ctypes.c_double)),
                 ("single_pass", ctypes.c_int),
                 ("single_pass_used", ctypes.POINTER(ctypes.c_int))]
+
+
+class odp_ttr_opts(ctypes.Structure):
+    _fields_ = [("eps", ctypes.c_double),
+                ("max_iters", ctypes.c_longlong),
+                ("big", ctypes.c_double),
+                ("stream", ctypes.c_void_p),
+                ("use_graph", ctypes.c_int),
+                ("iters_taken", ctypes.POINTER(ctypes.c_longlong)),
+                ("last_change", ctypes.POINTER(ctypes.c_double)),
+                ("kernel_ms", ctypes.POINTER(ctypes.c_double))]
 
 
 class OdpError(RuntimeError):
@@ -66,6 +77,10 @@ def _load():
         f = getattr(lib, name)
         f.argtypes = [vp, ctypes.c_int, D, ctypes.c_int, vp, D, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp,
                       ctypes.POINTER(odp_solve_opts)]
+        f.restype = ctypes.c_int
+    for name in ("odp_ttr_solve", "odp_ttr_solve_host"):
+        f = getattr(lib, name)
+        f.argtypes = [vp, ctypes.c_int, D, ctypes.c_int, vp, vp, ctypes.POINTER(odp_ttr_opts)]
         f.restype = ctypes.c_int
     lib.odp_partition_extent.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, I64, I64]
     lib.odp_partition_extent.restype = ctypes.c_int
@@ -262,3 +277,50 @@ def hj_solve_host(grid: Grid, dynamics: str, params, V0: np.ndarray, tau, accura
     if status != ODP_OK and raise_on_error:
         raise OdpError(status, last_error())
     return out, _info(keep, timing, status)
+
+
+def _ttr_opts(eps, max_iters, big, stream_ptr, use_graph):
+    o = odp_ttr_opts()
+    o.eps = float(eps)
+    o.max_iters = int(max_iters)
+    o.big = float(big)
+    o.stream = stream_ptr
+    o.use_graph = int(bool(use_graph))
+    it, ch, km = ctypes.c_longlong(), ctypes.c_double(), ctypes.c_double()
+    o.iters_taken = ctypes.pointer(it)
+    o.last_change = ctypes.pointer(ch)
+    o.kernel_ms = ctypes.pointer(km)
+    return o, (it, ch, km)
+
+
+def ttr_solve(grid: Grid, dynamics: str, params, V0, phi=None, eps: float = 1e-6, max_iters: int = 100000,
+              big: float = 100.0, stream=None, use_graph: bool = True):
+    """odp_ttr_solve (Algorithm 3) on torch CUDA tensors.  Returns (phi, info) with
+    info = {iters, last_change, kernel_ms}."""
+    import torch
+    assert V0.is_cuda and V0.dtype == torch.float32 and V0.is_contiguous() and V0.numel() == grid.points
+    if phi is None:
+        phi = torch.empty(tuple(grid.local_N), dtype=torch.float32, device=V0.device)
+    assert phi.is_cuda and phi.dtype == torch.float32 and phi.is_contiguous() and phi.numel() == grid.points
+    if stream is None:
+        stream = torch.cuda.current_stream(V0.device)
+    pa, pp = _dp(params)
+    o, (it, ch, km) = _ttr_opts(eps, max_iters, big, stream.cuda_stream, use_graph)
+    _check(_lib.odp_ttr_solve(grid.handle, DYNAMICS[dynamics], pp, len(pa), V0.data_ptr(), phi.data_ptr(),
+                              ctypes.byref(o)))
+    return phi, dict(iters=it.value, last_change=ch.value, kernel_ms=km.value)
+
+
+def ttr_solve_host(grid: Grid, dynamics: str, params, V0: np.ndarray, phi=None, eps: float = 1e-6,
+                   max_iters: int = 100000, big: float = 100.0, use_graph: bool = True):
+    """odp_ttr_solve_host: V0 / phi are host float32 arrays (copies inside the call)."""
+    V0 = np.ascontiguousarray(V0, dtype=np.float32)
+    assert V0.size == grid.points
+    if phi is None:
+        phi = np.empty(tuple(grid.local_N), dtype=np.float32)
+    assert phi.dtype == np.float32 and phi.flags["C_CONTIGUOUS"] and phi.size == grid.points
+    pa, pp = _dp(params)
+    o, (it, ch, km) = _ttr_opts(eps, max_iters, big, None, use_graph)
+    _check(_lib.odp_ttr_solve_host(grid.handle, DYNAMICS[dynamics], pp, len(pa), V0.ctypes.data, phi.ctypes.data,
+                                   ctypes.byref(o)))
+    return phi, dict(iters=it.value, last_change=ch.value, kernel_ms=km.value)

@@ -19,6 +19,7 @@
 
 #include "../../include/odp.h"
 #include "kernels_march.cuh"
+#include "kernels_ttr.cuh"
 
 using namespace odp;
 
@@ -487,6 +488,8 @@ struct odp_grid {
     cudaStream_t own_stream = nullptr;
     std::vector<cudaEvent_t> events;
     long long launches = 0;
+    TtrState *d_ttr = nullptr;    // time-to-reach iteration state (odp_ttr_solve)
+    TtrState *h_ttr = nullptr;    // pinned
 };
 
 static constexpr int R_MAX = 2;
@@ -500,6 +503,9 @@ static void free_device(odp_grid *g) {
     cudaFree(g->d_buf[0]); cudaFree(g->d_buf[1]);
     cudaFree(g->d_partials); cudaFree(g->d_state); cudaFree(g->d_range); cudaFree(g->d_amax);
     if (g->h_state) cudaFreeHost(g->h_state);
+    cudaFree(g->d_ttr);
+    if (g->h_ttr) cudaFreeHost(g->h_ttr);
+    g->d_ttr = nullptr; g->h_ttr = nullptr;
     if (g->own_stream) cudaStreamDestroy(g->own_stream);
     for (auto e : g->events) cudaEventDestroy(e);
     g->events.clear();
@@ -719,8 +725,7 @@ static odp_status range_allreduce(odp_grid *g, int n, cudaStream_t s) {
 static const int kWantParams[7] = {2, 3, 3, 5, 3, 3, 5};
 static const int kWantDims[7] = {0, 0, 3, 4, 5, 6, 3};
 
-static odp_status validate(const odp_grid *g, int dyn, const double *params, int nparams, const double *tau,
-                           int ntau, int accuracy, int mode) {
+static odp_status validate_dyn(const odp_grid *g, int dyn, const double *params, int nparams) {
     if (!g) return fail(ODP_EINVAL, "NULL grid");
     if (dyn < 0 || dyn > 6) return fail(ODP_EINVAL, "unknown dynamics id %d", dyn);
     if (!params || nparams != kWantParams[dyn]) return fail(ODP_EINVAL, "dynamics %d takes %d params (got %d)", dyn, kWantParams[dyn], nparams);
@@ -728,6 +733,13 @@ static odp_status validate(const odp_grid *g, int dyn, const double *params, int
     const double goal = params[nparams - 1];
     if (goal != 1.0 && goal != -1.0) return fail(ODP_EINVAL, "goal must be -1 or +1");
     for (int k = 0; k < nparams; ++k) if (!std::isfinite(params[k])) return fail(ODP_EINVAL, "param %d not finite", k);
+    return ODP_OK;
+}
+
+static odp_status validate(const odp_grid *g, int dyn, const double *params, int nparams, const double *tau,
+                           int ntau, int accuracy, int mode) {
+    odp_status st = validate_dyn(g, dyn, params, nparams);
+    if (st) return st;
     if (accuracy != ODP_LOW && accuracy != ODP_MEDIUM) return fail(ODP_EINVAL, "accuracy %d", accuracy);
     if (mode != ODP_BRS && mode != ODP_BRT) return fail(ODP_EINVAL, "mode %d", mode);
     if (!tau || ntau < 2) return fail(ODP_EINVAL, "need ntau >= 2");
@@ -1090,6 +1102,173 @@ extern "C" odp_status odp_hj_solve_host(odp_grid *g, int dynamics_id, const doub
     cudaFreeAsync(dV0, s);
     cudaFreeAsync(dout, s);
     if (dT) cudaFreeAsync(dT, s);
+    cudaStreamSynchronize(s);
+    return st;
+}
+
+// ------------------------------------------------------------------------------------------------
+// time-to-reach (Algorithm 3; readings A31-A35)
+// ------------------------------------------------------------------------------------------------
+template <template <int> class FH>
+static TtrFns ttr_holo(int n) {
+    switch (n) {
+    case 1: return ttr_fns<FH<1>, 1>();
+    case 2: return ttr_fns<FH<2>, 2>();
+    case 3: return ttr_fns<FH<3>, 3>();
+    case 4: return ttr_fns<FH<4>, 4>();
+    case 5: return ttr_fns<FH<5>, 5>();
+    default: return ttr_fns<FH<6>, 6>();
+    }
+}
+
+static TtrFns ttr_select(int dyn, int n) {
+    switch (dyn) {
+    case ODP_DYN_HOLONOMIC_BALL: return ttr_holo<FHoloBall>(n);
+    case ODP_DYN_HOLONOMIC_BOX: return ttr_holo<FHoloBox>(n);
+    case ODP_DYN_DUBINS3D: return ttr_fns<FDubins3D, 3>();
+    case ODP_DYN_CAR4D: return ttr_fns<FCar4D, 4>();
+    case ODP_DYN_CAR5D: return ttr_fns<FCar5D, 5>();
+    case ODP_DYN_PAIR_DUBINS3D: return ttr_fns<FPairDubins3D, 3>();
+    default: return ttr_fns<FDoubleInt6D, 6>();
+    }
+}
+
+static odp_status ttr_device(odp_grid *g, int dyn, const double *params, int nparams, const float *V0, float *phi,
+                             const odp_ttr_opts *opts) {
+    odp_status st = validate_dyn(g, dyn, params, nparams);
+    if (st) return st;
+    if (!V0 || !phi) return fail(ODP_EINVAL, "NULL V0/phi");
+    if (V0 == phi) return fail(ODP_EINVAL, "phi aliases V0");
+    if (g->nranks > 1 || g->comm) return fail(ODP_EINVAL, "time-to-reach runs on an unpartitioned grid");
+    for (int d = 0; d < g->n; ++d)
+        if (!g->per[d] && g->N[d] < 4) return fail(ODP_EINVAL, "N[%d]=%lld < 4 on a non-periodic axis", d, (long long)g->N[d]);
+    const double eps = (opts && opts->eps > 0.0) ? opts->eps : 1e-6;
+    const long long max_iters = (opts && opts->max_iters > 0) ? opts->max_iters : 100000;
+    const double big = (opts && opts->big > 0.0) ? opts->big : 100.0;
+    const bool use_graph = opts ? opts->use_graph != 0 : true;
+    if ((st = ensure_device(g, 1))) return st;
+    if (!g->d_ttr) {
+        CUDA_TRY(cudaMalloc(&g->d_ttr, sizeof(TtrState)));
+        CUDA_TRY(cudaMallocHost(&g->h_ttr, sizeof(TtrState)));
+    }
+    cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
+    const int n = g->n;
+    const TtrFns fn = ttr_select(dyn, n);
+    GridDev gd = make_griddev(g);
+    FParams fp;
+    memset(&fp, 0, sizeof fp);
+    for (int k = 0; k < nparams; ++k) fp.c[k] = (float)params[k];
+    fp.c[nparams - 1] = -1.f;                                   // A32: the control minimises p.f
+    int nsm = 148, dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int block = 256;
+    const long long P = local_points(g);
+    const int grid_all = (int)std::min<long long>((P + block - 1) / block, (long long)nsm * 8);
+    int grid_face[MAXD] = {0};
+    for (int d = 0; d < n; ++d)
+        grid_face[d] = (int)std::min<long long>((2 * (P / g->N[d]) + block - 1) / block, (long long)nsm * 8);
+    float *buf[2] = {phi, g->d_buf[0] + g->halo_elems};
+    g->launches = 0;
+
+    k_ttr_reset<<<1, 1, 0, s>>>(g->d_ttr, max_iters, (float)eps);
+    k_ttr_init<<<grid_all, block, 0, s>>>(P, V0, (float)big, buf[0]);
+    g->launches += 2;
+    CUDA_TRY(cudaGetLastError());
+    const int G = 16;                                           // iterations per chunk (even)
+    int per_iter = 2;
+    for (int d = 0; d < n; ++d) per_iter += g->per[d] ? 0 : 1;
+    auto chunk = [&](void) -> cudaError_t {
+        for (int k = 0; k < G; ++k) {
+            const int par = (k + 1) & 1;
+            const float *src = buf[k & 1];
+            float *dst = buf[par];
+            fn.interior<<<grid_all, block, 0, s>>>(gd, fp, V0, src, dst, g->d_ttr, par);
+            for (int d = 0; d < n; ++d)
+                if (!g->per[d]) fn.face<<<grid_face[d], block, 0, s>>>(gd, d, src, dst, g->d_ttr, par);
+            k_ttr_ctl<<<1, 1, 0, s>>>(g->d_ttr, par);
+        }
+        return cudaGetLastError();
+    };
+    cudaGraphExec_t exec = nullptr;
+    if (use_graph) {
+        cudaGraph_t graph = nullptr;
+        CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        cudaError_t e = chunk();
+        cudaError_t e2 = cudaStreamEndCapture(s, &graph);
+        if (e != cudaSuccess || e2 != cudaSuccess) {
+            if (graph) cudaGraphDestroy(graph);
+            return fail(ODP_ECUDA, "graph capture: %s", cudaGetErrorString(e != cudaSuccess ? e : e2));
+        }
+        e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return fail(ODP_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    }
+    cudaEvent_t ev[2];
+    CUDA_TRY(cudaEventCreate(&ev[0]));
+    CUDA_TRY(cudaEventCreate(&ev[1]));
+    double ms_total = 0.0;
+    odp_status rs = ODP_OK;
+    for (;;) {
+        cudaError_t e = cudaEventRecord(ev[0], s);
+        if (e == cudaSuccess) e = use_graph ? cudaGraphLaunch(exec, s) : chunk();
+        if (e == cudaSuccess) e = cudaEventRecord(ev[1], s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(g->h_ttr, g->d_ttr, sizeof(TtrState), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) { rs = fail(ODP_ECUDA, "ttr iteration: %s", cudaGetErrorString(e)); break; }
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[0], ev[1]);
+        ms_total += ms;
+        g->launches += (long long)G * per_iter;
+        if (g->h_ttr->done) break;
+    }
+    if (exec) cudaGraphExecDestroy(exec);
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    if (rs) return rs;
+    if (g->h_ttr->parity == 1) {
+        CUDA_TRY(cudaMemcpyAsync(phi, buf[1], (size_t)P * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    if (opts) {
+        if (opts->iters_taken) *opts->iters_taken = g->h_ttr->iters;
+        if (opts->last_change) *opts->last_change = (double)__builtin_bit_cast(float, g->h_ttr->change[g->h_ttr->parity]);
+        if (opts->kernel_ms) *opts->kernel_ms = ms_total;
+    }
+    return ODP_OK;
+}
+
+extern "C" odp_status odp_ttr_solve(odp_grid *g, int dynamics_id, const double *params, int nparams,
+                                    const float *V0, float *phi, const odp_ttr_opts *opts) {
+    g_err.clear();
+    return ttr_device(g, dynamics_id, params, nparams, V0, phi, opts);
+}
+
+extern "C" odp_status odp_ttr_solve_host(odp_grid *g, int dynamics_id, const double *params, int nparams,
+                                         const float *V0, float *phi, const odp_ttr_opts *opts) {
+    g_err.clear();
+    odp_status st = validate_dyn(g, dynamics_id, params, nparams);
+    if (st) return st;
+    if (!V0 || !phi) return fail(ODP_EINVAL, "NULL V0/phi");
+    if ((st = ensure_device(g, 1))) return st;
+    const size_t bytes = (size_t)local_points(g) * sizeof(float);
+    cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
+    float *dV0 = nullptr, *dphi = nullptr;
+    CUDA_TRY(cudaMallocAsync(&dV0, bytes, s));
+    CUDA_TRY(cudaMallocAsync(&dphi, bytes, s));
+    odp_ttr_opts o;
+    memset(&o, 0, sizeof o);
+    if (opts) o = *opts; else o.use_graph = 1;
+    o.stream = s;
+    CUDA_TRY(cudaMemcpyAsync(dV0, V0, bytes, cudaMemcpyHostToDevice, s));
+    st = ttr_device(g, dynamics_id, params, nparams, dV0, dphi, &o);
+    if (st == ODP_OK) {
+        cudaError_t e = cudaMemcpyAsync(phi, dphi, bytes, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = fail(ODP_ECUDA, "copy out: %s", cudaGetErrorString(e));
+    }
+    cudaFreeAsync(dV0, s);
+    cudaFreeAsync(dphi, s);
     cudaStreamSynchronize(s);
     return st;
 }

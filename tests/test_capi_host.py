@@ -80,3 +80,23 @@ def test_unknown_dynamics(capi):
                                  1, 1, ctypes.c_void_p(32), None)
     assert st == capi.ODP_EINVAL and "unknown dynamics" in capi.last_error()
     g.close()
+
+
+@pytest.mark.parametrize("N,per,kw,msg", [
+    ((5, 5), 0, dict(dynamics="DUBINS3D", params=(1, 1, -1)), "needs dims"),
+    ((5, 5), 0, dict(params=(1.0, 0.2)), "params"),
+    ((5, 5), 0, dict(params=(1.0, 0.2, 0.0)), "goal"),
+    ((5, 3), 0, {}, "N[1]=3 < 4"),
+    ((5, 5), 0, dict(alias=True), "aliases"),
+])
+def test_ttr_validation_before_device_work(capi, N, per, kw, msg):
+    g = capi.Grid(N, (-1, -1), (1, 1), per)
+    a = dict(dynamics="HOLONOMIC_BOX", params=(1.0, 0.2, -1.0))
+    a.update(kw)
+    pa = np.ascontiguousarray(a["params"], dtype=np.float64)
+    out = ctypes.c_void_p(16 if a.get("alias") else 32)
+    st = capi.lib().odp_ttr_solve(g.handle, capi.DYNAMICS[a["dynamics"]], pa.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                  len(pa), ctypes.c_void_p(16), out, None)
+    assert st == capi.ODP_EINVAL
+    assert msg in capi.last_error()
+    g.close()
