@@ -5,17 +5,23 @@
 // A sequential in-place sweep has no parallelism across the grid, so the GPU path iterates the
 // same update as a Jacobi iteration (reading A35): every node of iteration k+1 is computed from
 // iteration k, then the boundary rule of l.14-15 is applied along each non-periodic axis in order
-// 0..n-1 (reading A34).  One iteration = one k_ttr_interior launch + one k_ttr_face launch per
-// non-periodic axis + k_ttr_ctl; buffers alternate, the convergence test (A31) runs on the device.
+// 0..n-1 (reading A34).  Buffers alternate and the convergence test
+// (A31) runs on the device.  One iteration = 1 + (non-periodic axes) launches:
 //
 //   k_ttr_init      l.1: phi = 0 on the target {V0 <= 0}, `big` elsewhere
-//   k_ttr_interior  l.5-12 for every node not on a non-periodic face (A32, A33)
-//   k_ttr_face<d>   l.14-15 along axis d on its two faces
-//   k_ttr_ctl       l.2 (A31): stop once max |phi_new - phi_old| <= eps (or the iteration cap)
+//   k_ttr_rows      l.5-12 on every node not on a non-periodic face (A32, A33); one CTA row group
+//                   per iteration of its loop: the row's coordinates, face flags and index
+//                   arithmetic are uniform, the innermost axis runs across the threads
+//   k_ttr_face<d>   l.14-15 along non-periodic axis d on its two faces, in place, axes in order;
+//                   the last CTA of the iteration's last launch runs l.2's stop test
+//   k_ttr_finish    writes +0 over the target marker
+//
+// The target is carried in the value itself: a target node holds -0.0f (l.1, A34: never updated),
+// every other node a value whose sign bit is clear (neighbour reads go through |x|, results are
+// normalised with + 0.0f), so the iteration reads 8 bytes per node instead of 12 (no V0 stream).
 #pragma once
 
 #include "odp_device.cuh"
-#include "kernels_generic.cuh"
 
 namespace odp {
 
@@ -26,8 +32,10 @@ struct TtrState {
     long long iters;      // iterations executed
     long long max_iters;
     float eps;
-    int pad;
+    unsigned blocks_done; // CTAs of the current k_ttr_faces launch that finished
 };
+
+__device__ __forceinline__ bool is_target(float v) { return __float_as_uint(v) == 0x80000000u; }
 
 __device__ __forceinline__ void ttr_reduce_change(float c, TtrState *st, int par) {
 #pragma unroll
@@ -36,25 +44,132 @@ __device__ __forceinline__ void ttr_reduce_change(float c, TtrState *st, int par
     if ((threadIdx.x & 31) == 0 && c > 0.f) atomicMax(&st->change[par], __float_as_uint(c));
 }
 
+// Stop test of l.2 (A31) for the iteration that wrote `par`, run by the last CTA of the iteration's
+// last launch: every CTA's atomicMax is visible after its fence + counter increment.
+__device__ __forceinline__ void ttr_last_cta_control(TtrState *st, int par) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&st->blocks_done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        st->blocks_done = 0u;
+        st->iters += 1;
+        const float c = __uint_as_float(atomicAdd(&st->change[par], 0u));
+        if (c <= st->eps || st->iters >= st->max_iters) { st->done = 1; st->parity = par; }
+        else st->change[par ^ 1] = 0u;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_ttr_init(long long P, const float *__restrict__ V0, float big,
                                                   float *__restrict__ phi) {
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += stride)
-        phi[i] = __ldg(V0 + i) <= 0.f ? 0.f : big;                      // l.1
+        phi[i] = __ldg(V0 + i) <= 0.f ? -0.f : big;                     // l.1 (target marker -0)
+}
+
+__global__ void __launch_bounds__(256) k_ttr_finish(long long P, const float *src, float *phi) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += stride)
+        phi[i] = fabsf(src[i]);                                           // -0 target marker -> 0
 }
 
 __global__ void k_ttr_reset(TtrState *st, long long max_iters, float eps) {
     st->change[0] = st->change[1] = 0u;
     st->done = 0; st->parity = 0; st->iters = 0;
     st->max_iters = max_iters; st->eps = eps;
+    st->blocks_done = 0u;
 }
 
-// l.5-12 on every node; face nodes of non-periodic axes are copied (their value comes from
-// k_ttr_face).  Reads src (iteration k), writes dst (iteration k+1).
+// l.5-12.  Rows = all axes but the innermost; RPB = rows per CTA step (blockDim / N_last, >= 1).
 template <class F, int NDIM>
-__global__ void __launch_bounds__(256) k_ttr_interior(GridDev g, FParams fp, const float *__restrict__ V0,
-                                                      const float *__restrict__ src, float *__restrict__ dst,
-                                                      TtrState *st, int par) {
+__global__ void __launch_bounds__(256) k_ttr_rows(GridDev g, FParams fp, const float *__restrict__ src,
+                                                  float *__restrict__ dst, TtrState *st, int par, int last_launch) {
+    if (st->done) return;
+    constexpr int L = NDIM - 1;
+    F f;
+    {
+        float mn[MAXD], mx[MAXD];
+#pragma unroll
+        for (int d = 0; d < MAXD; ++d) { mn[d] = -1.f; mx[d] = 1.f; }        // A33: costate box [-1, 1]^n
+        f.init(fp, mn, mx);
+    }
+    const int NL = g.N[L];
+    const int RPB = NL >= (int)blockDim.x ? 1 : (int)blockDim.x / NL;
+    const int lr = NL >= (int)blockDim.x ? 0 : (int)threadIdx.x / NL;
+    const int j0 = NL >= (int)blockDim.x ? (int)threadIdx.x : (int)threadIdx.x - lr * NL;
+    const long long rows = g.P / NL;
+    const bool perL = g.per[L] != 0;
+    float cmax = 0.f;
+    if (lr < RPB) {
+        for (long long rg = blockIdx.x; rg * RPB < rows; rg += gridDim.x) {
+            const long long r = rg * RPB + lr;
+            if (r >= rows) break;
+            int idx[NDIM];
+            bool row_face = false;
+            {
+                long long rr = r;
+#pragma unroll
+                for (int d = L - 1; d >= 1; --d) {
+                    const long long qd = rr / g.N[d];
+                    idx[d] = (int)(rr - qd * g.N[d]);
+                    rr = qd;
+                }
+                idx[0] = (int)rr;
+#pragma unroll
+                for (int d = 0; d < L; ++d) row_face |= !g.per[d] && (idx[d] == 0 || idx[d] == g.N[d] - 1);
+            }
+            const long long base = r * NL;
+            if (row_face) {                              // A34: faces take l.14-15 in k_ttr_face
+                for (int j = j0; j < NL; j += blockDim.x) dst[base + j] = src[base + j];
+                continue;
+            }
+            Pt q;
+#pragma unroll
+            for (int d = 0; d < L; ++d) load_axis<F>(g, q, d, idx[d]);
+            for (int j = j0; j < NL; j += blockDim.x) {
+                const long long i = base + j;
+                const float old = src[i];
+                if (is_target(old) || (!perL && (j == 0 || j == NL - 1))) { dst[i] = old; continue; }   // A34
+                idx[L] = j;
+                load_axis<F>(g, q, L, j);
+                float p[NDIM];
+                float num = 0.f, den = 0.f;
+#pragma unroll
+                for (int d = 0; d < NDIM; ++d) {
+                    const long long s = g.stride[d];
+                    long long op = s, om = -s;
+                    if (g.per[d]) {                      // periodic wrap (interior nodes never wrap otherwise)
+                        if (idx[d] == g.N[d] - 1) op = -(long long)(g.N[d] - 1) * s;
+                        if (idx[d] == 0) om = (long long)(g.N[d] - 1) * s;
+                    }
+                    const float vp = fabsf(src[i + op]), vm = fabsf(src[i + om]);
+                    p[d] = (vp - vm) * g.hih[d];         // central difference (A32)
+                    const float a = f.alpha(d, q);
+                    num = fmaf(a * g.hih[d], vp + vm, num);
+                    den = fmaf(a, g.inv_dx[d], den);
+                }
+                const float H = -f.ham(q, p) - 1.f;      // A32: H_TTR = -H_reach(goal -1) - 1
+                const float nv = den > 0.f ? (num - H) / den : old;     // l.10-11 (A33)
+                const float v = fminf(nv, old) + 0.f;    // l.12 (+0: never the target marker)
+                dst[i] = v;
+                cmax = fmaxf(cmax, fabsf(v - old));
+            }
+        }
+    }
+    ttr_reduce_change(cmax, st, par);
+    if (last_launch) ttr_last_cta_control(st, par);
+}
+
+// l.5-12 for NDIM >= 2: thread = one column (fixed indices of axes 1..n-1, consecutive threads =
+// consecutive addresses of an axis-0 plane), marching axis 0 over one segment of planes
+// (blockIdx.y) with the axis-0 neighbours in a register window.  Per-column work (index
+// decomposition, coordinates, wrapped neighbour offsets, face test) is done once per column.
+template <class F, int NDIM>
+__global__ void __launch_bounds__(256) k_ttr_march(GridDev g, FParams fp, const float *__restrict__ src,
+                                                   float *__restrict__ dst, TtrState *st, int par, int last_launch,
+                                                   int seg_len) {
     if (st->done) return;
     F f;
     {
@@ -63,54 +178,113 @@ __global__ void __launch_bounds__(256) k_ttr_interior(GridDev g, FParams fp, con
         for (int d = 0; d < MAXD; ++d) { mn[d] = -1.f; mx[d] = 1.f; }        // A33: costate box [-1, 1]^n
         f.init(fp, mn, mx);
     }
+    const int ncol = (int)g.stride[0];
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int N0 = g.N[0];
+    const int a0 = blockIdx.y * seg_len, a1 = min(N0, a0 + seg_len);
     float cmax = 0.f;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.P; i += stride) {
+    if (c < ncol) {
         int idx[NDIM];
-        node_index<NDIM>(g, i, idx);
-        const float old = src[i];
-        bool face = false;
+        bool col_face = false;
+        int op[NDIM], om[NDIM];
+        {
+            int rem = c;
 #pragma unroll
-        for (int d = 0; d < NDIM; ++d) face |= !g.per[d] && (idx[d] == 0 || idx[d] == g.N[d] - 1);
-        if (face || __ldg(V0 + i) <= 0.f) { dst[i] = old; continue; }     // A34: faces later, target fixed
-        Pt q;
-        float p[NDIM];
-        float num = 0.f, den = 0.f;
-#pragma unroll
-        for (int d = 0; d < NDIM; ++d) load_axis<F>(g, q, d, idx[d]);   // alpha_d may read any axis
-#pragma unroll
-        for (int d = 0; d < NDIM; ++d) {
-            const long long s = g.stride[d];
-            long long op = s, om = -s;
-            if (g.per[d]) {                              // periodic wrap (interior nodes never wrap otherwise)
-                if (idx[d] == g.N[d] - 1) op = -(long long)(g.N[d] - 1) * s;
-                if (idx[d] == 0) om = (long long)(g.N[d] - 1) * s;
+            for (int d = NDIM - 1; d >= 1; --d) {
+                const int q = rem / g.N[d];
+                idx[d] = rem - q * g.N[d];
+                rem = q;
+                const int sd = (int)g.stride[d];
+                op[d] = sd; om[d] = -sd;
+                if (g.per[d]) {
+                    if (idx[d] == g.N[d] - 1) op[d] = -(g.N[d] - 1) * sd;
+                    if (idx[d] == 0) om[d] = (g.N[d] - 1) * sd;
+                } else if (idx[d] == 0 || idx[d] == g.N[d] - 1) {
+                    col_face = true;
+                }
             }
-            const float vp = src[i + op], vm = src[i + om];
-            p[d] = (vp - vm) * g.hih[d];                 // central difference (A32)
-            num = fmaf(f.alpha(d, q) * g.hih[d], vp + vm, num);
-            den = fmaf(f.alpha(d, q), g.inv_dx[d], den);
         }
-        const float H = -f.ham(q, p) - 1.f;              // A32: H_TTR = -H_reach(goal -1) - 1
-        const float nv = den > 0.f ? (num - H) / den : old;    // l.10-11 (A33)
-        const float v = fminf(nv, old);                  // l.12
-        dst[i] = v;
-        cmax = fmaxf(cmax, fabsf(v - old));
+        const long long s0 = (long long)ncol;
+        if (col_face) {                                  // A34: faces take l.14-15 in k_ttr_face
+            for (int i0 = a0; i0 < a1; ++i0) dst[i0 * s0 + c] = src[i0 * s0 + c];
+        } else {
+            Pt q;
+#pragma unroll
+            for (int d = 1; d < NDIM; ++d) load_axis<F>(g, q, d, idx[d]);
+            const bool per0 = g.per[0] != 0;
+            const float *col = src + c;
+            auto at0 = [&](int i0) -> float {            // phi at plane i0 (wrapped if periodic)
+                if (per0) i0 = i0 < 0 ? i0 + N0 : (i0 >= N0 ? i0 - N0 : i0);
+                else i0 = max(0, min(N0 - 1, i0));
+                return col[i0 * s0];
+            };
+            // U planes per batch: all loads of a batch are issued before its arithmetic (the
+            // side-neighbour loads come from L2; the batch keeps U of them in flight per thread)
+            constexpr int U = 4;
+            float vm = fabsf(at0(a0 - 1)), vc = at0(a0);
+            for (int ib = a0; ib < a1; ib += U) {
+                float vn[U], sp[U][NDIM], sm[U][NDIM];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (ib + u < a1) {
+                        vn[u] = at0(ib + u + 1);
+                        const float *pc = col + (long long)(ib + u) * s0;
+#pragma unroll
+                        for (int d = 1; d < NDIM; ++d) { sp[u][d] = pc[op[d]]; sm[u][d] = pc[om[d]]; }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (ib + u >= a1) break;
+                    const int i0 = ib + u;
+                    const long long i = i0 * s0 + c;
+                    const float old = vc;
+                    if (is_target(old) || (!per0 && (i0 == 0 || i0 == N0 - 1))) {
+                        dst[i] = old;                    // A34
+                    } else {
+                        load_axis<F>(g, q, 0, i0);
+                        float p[NDIM];
+                        const float vp0 = fabsf(vn[u]);
+                        p[0] = (vp0 - vm) * g.hih[0];    // central difference (A32)
+                        const float a0v = f.alpha(0, q);
+                        float num = a0v * g.hih[0] * (vp0 + vm);
+                        float den = a0v * g.inv_dx[0];
+#pragma unroll
+                        for (int d = 1; d < NDIM; ++d) {
+                            const float vp = fabsf(sp[u][d]), vmd = fabsf(sm[u][d]);
+                            p[d] = (vp - vmd) * g.hih[d];
+                            const float a = f.alpha(d, q);
+                            num = fmaf(a * g.hih[d], vp + vmd, num);
+                            den = fmaf(a, g.inv_dx[d], den);
+                        }
+                        const float H = -f.ham(q, p) - 1.f;   // A32: H_TTR = -H_reach(goal -1) - 1
+                        const float nv = den > 0.f ? (num - H) / den : old;   // l.10-11 (A33)
+                        const float v = fminf(nv, old) + 0.f;               // l.12
+                        dst[i] = v;
+                        cmax = fmaxf(cmax, fabsf(v - old));
+                    }
+                    vm = fabsf(vc);
+                    vc = vn[u];
+                }
+            }
+        }
     }
     ttr_reduce_change(cmax, st, par);
+    if (last_launch) ttr_last_cta_control(st, par);
 }
 
-// l.14-15 along axis d: phi_face = min(max(2 phi_1 - phi_2, phi_2), phi_face) on both faces, from
-// the values already in dst (after the interior update and the rules of axes < d).  Nodes whose
-// highest non-periodic face axis is d are final here and enter the change.
+// l.14-15 along axis d on its two faces, in place in dst (which holds the interior update and the
+// rules of axes < d; face nodes were copied from src by k_ttr_rows).  The rule reads the nodes 1 and
+// 2 cells inside, never on an axis-d face (N >= 4), so no value this launch writes is read.  Nodes
+// whose highest non-periodic face axis is d are final and enter the change.
 template <int NDIM>
-__global__ void __launch_bounds__(256) k_ttr_face(GridDev g, int d, const float *__restrict__ src, float *dst,
-                                                  TtrState *st, int par) {
+__global__ void __launch_bounds__(256) k_ttr_face(GridDev g, int d, int last_launch, const float *__restrict__ src,
+                                                  float *dst, TtrState *st, int par) {
     if (st->done) return;
     const long long inner = g.stride[d];
-    const long long outer = g.P / (inner * g.N[d]);
-    const long long per_side = outer * inner;
     const int Nd = g.N[d];
+    const long long outer = g.P / (inner * Nd);
+    const long long per_side = outer * inner;
     float cmax = 0.f;
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * per_side; t += stride) {
@@ -118,42 +292,47 @@ __global__ void __launch_bounds__(256) k_ttr_face(GridDev g, int d, const float 
         const long long r = side ? t - per_side : t;
         const long long o = r / inner, in = r - o * inner;
         const long long i = o * (inner * Nd) + (side ? (long long)(Nd - 1) * inner : 0) + in;
-        const long long sa = side ? -inner : inner;
-        const float a = dst[i + sa], b = dst[i + 2 * sa], cur = dst[i];
-        const float v = fminf(fmaxf(2.f * a - b, b), cur);
-        dst[i] = v;
-        int idx[NDIM];
-        node_index<NDIM>(g, i, idx);
+        const float cur = dst[i];
+        float v = cur;
+        if (!is_target(cur)) {                           // A34: target nodes keep 0
+            const long long sa = side ? -inner : inner;
+            const float a = fabsf(dst[i + sa]), b = fabsf(dst[i + 2 * sa]);
+            v = fminf(fmaxf(2.f * a - b, b), cur) + 0.f;
+            dst[i] = v;
+        }
+        // highest face axis of this node: the axes e > d are decoded from `in`
         bool last = true;
+        long long rem = in;
 #pragma unroll
-        for (int e = 0; e < NDIM; ++e)
-            if (e > d && !g.per[e] && (idx[e] == 0 || idx[e] == g.N[e] - 1)) last = false;
+        for (int e = NDIM - 1; e > 0; --e) {
+            if (e <= d) break;
+            const long long q = rem / g.N[e];
+            const int ie = (int)(rem - q * g.N[e]);
+            rem = q;
+            if (!g.per[e] && (ie == 0 || ie == g.N[e] - 1)) last = false;
+        }
         if (last) cmax = fmaxf(cmax, fabsf(v - src[i]));
     }
     ttr_reduce_change(cmax, st, par);
+    if (last_launch) ttr_last_cta_control(st, par);
 }
 
-// l.2 (A31): the iteration that wrote parity `par` is done; stop when its change <= eps.
-__global__ void k_ttr_ctl(TtrState *st, int par) {
-    if (st->done) return;
-    st->iters += 1;
-    const float c = __uint_as_float(st->change[par]);
-    if (c <= st->eps || st->iters >= st->max_iters) { st->done = 1; st->parity = par; return; }
-    st->change[par ^ 1] = 0u;
-}
+typedef void (*ttr_rows_fn)(GridDev, FParams, const float *, float *, TtrState *, int, int);
+typedef void (*ttr_face_fn)(GridDev, int, int, const float *, float *, TtrState *, int);
 
-typedef void (*ttr_interior_fn)(GridDev, FParams, const float *, const float *, float *, TtrState *, int);
-typedef void (*ttr_face_fn)(GridDev, int, const float *, float *, TtrState *, int);
+typedef void (*ttr_march_fn)(GridDev, FParams, const float *, float *, TtrState *, int, int, int);
 
 struct TtrFns {
-    ttr_interior_fn interior = nullptr;
+    ttr_rows_fn rows = nullptr;       // NDIM == 1
+    ttr_march_fn march = nullptr;     // NDIM >= 2
     ttr_face_fn face = nullptr;
 };
 
 template <class F, int NDIM>
 static TtrFns ttr_fns() {
     TtrFns t;
-    t.interior = k_ttr_interior<F, NDIM>;
+    if constexpr (NDIM == 1) t.rows = k_ttr_rows<F, NDIM>;
+    else t.march = k_ttr_march<F, NDIM>;
     t.face = k_ttr_face<NDIM>;
     return t;
 }

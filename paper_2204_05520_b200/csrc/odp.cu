@@ -1165,9 +1165,22 @@ static odp_status ttr_device(odp_grid *g, int dyn, const double *params, int npa
     const int block = 256;
     const long long P = local_points(g);
     const int grid_all = (int)std::min<long long>((P + block - 1) / block, (long long)nsm * 8);
-    int grid_face[MAXD] = {0};
-    for (int d = 0; d < n; ++d)
+    const int NL = (int)g->N[n - 1];
+    const long long rows = P / NL;
+    const int RPB = NL >= block ? 1 : block / NL;
+    const int grid_rows = (int)std::min<long long>((rows + RPB - 1) / RPB, (long long)nsm * 8);
+    // march kernel: columns = one axis-0 plane; axis 0 split into segments so that ~8 CTAs per SM run
+    const long long ncol = P / g->n0;
+    const int col_blocks = (int)((ncol + block - 1) / block);
+    int nseg = (int)std::max<long long>(1, std::min<long long>(g->n0, ((long long)nsm * 8 + col_blocks - 1) / col_blocks));
+    const int seg_len = (int)((g->n0 + nseg - 1) / nseg);
+    nseg = (int)((g->n0 + seg_len - 1) / seg_len);
+    const dim3 grid_march(col_blocks, nseg);
+    int grid_face[MAXD] = {0}, last_axis = -1;
+    for (int d = 0; d < n; ++d) {
         grid_face[d] = (int)std::min<long long>((2 * (P / g->N[d]) + block - 1) / block, (long long)nsm * 8);
+        if (!g->per[d]) last_axis = d;
+    }
     float *buf[2] = {phi, g->d_buf[0] + g->halo_elems};
     g->launches = 0;
 
@@ -1176,17 +1189,16 @@ static odp_status ttr_device(odp_grid *g, int dyn, const double *params, int npa
     g->launches += 2;
     CUDA_TRY(cudaGetLastError());
     const int G = 16;                                           // iterations per chunk (even)
-    int per_iter = 2;
-    for (int d = 0; d < n; ++d) per_iter += g->per[d] ? 0 : 1;
+    const int per_iter = 1 + [&] { int c = 0; for (int d = 0; d < n; ++d) c += g->per[d] ? 0 : 1; return c; }();
     auto chunk = [&](void) -> cudaError_t {
         for (int k = 0; k < G; ++k) {
             const int par = (k + 1) & 1;
             const float *src = buf[k & 1];
             float *dst = buf[par];
-            fn.interior<<<grid_all, block, 0, s>>>(gd, fp, V0, src, dst, g->d_ttr, par);
+            if (fn.march) fn.march<<<grid_march, block, 0, s>>>(gd, fp, src, dst, g->d_ttr, par, last_axis < 0 ? 1 : 0, seg_len);
+            else fn.rows<<<grid_rows, block, 0, s>>>(gd, fp, src, dst, g->d_ttr, par, last_axis < 0 ? 1 : 0);
             for (int d = 0; d < n; ++d)
-                if (!g->per[d]) fn.face<<<grid_face[d], block, 0, s>>>(gd, d, src, dst, g->d_ttr, par);
-            k_ttr_ctl<<<1, 1, 0, s>>>(g->d_ttr, par);
+                if (!g->per[d]) fn.face<<<grid_face[d], block, 0, s>>>(gd, d, d == last_axis ? 1 : 0, src, dst, g->d_ttr, par);
         }
         return cudaGetLastError();
     };
@@ -1226,10 +1238,10 @@ static odp_status ttr_device(odp_grid *g, int dyn, const double *params, int npa
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
     if (rs) return rs;
-    if (g->h_ttr->parity == 1) {
-        CUDA_TRY(cudaMemcpyAsync(phi, buf[1], (size_t)P * sizeof(float), cudaMemcpyDeviceToDevice, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
-    }
+    k_ttr_finish<<<grid_all, block, 0, s>>>(P, buf[g->h_ttr->parity], phi);
+    g->launches += 1;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(s));
     if (opts) {
         if (opts->iters_taken) *opts->iters_taken = g->h_ttr->iters;
         if (opts->last_change) *opts->last_change = (double)__builtin_bit_cast(float, g->h_ttr->change[g->h_ttr->parity]);
