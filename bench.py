@@ -8,6 +8,9 @@ N=1 workload: c4 (6D double integrator, 30^6 = 7.29e8 points, ENO2 + TVD-RK2, BR
 the largest config that fits one GPU and the one BASELINE.json's scaling target names.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+--config t1 measures SURVEY.md §8(f3) instead: time-to-reach (Algorithm 3) on the Dubins car at 256^3,
+a step = one odp_ttr_solve to convergence, value = node updates (nodes x iterations) / device time.
 """
 from __future__ import annotations
 
@@ -141,6 +144,173 @@ def oracle_sample(w, target_s: float = 15.0):
     sample = (f"oracle float64 on a {'x'.join(map(str, sub.N))} centred sub-box of {w.name} (same spacing, "
               f"dynamics, target), one time step = {stages} RK stages, {el:.1f} s")
     return work / el, sample, cores, el, work
+
+
+# --------------------------------------------------------------------------------------------------
+# time-to-reach (Algorithm 3) -- a step is one odp_ttr_solve to convergence
+# --------------------------------------------------------------------------------------------------
+TTR_METRIC = "TTR node updates/s (Lax-Friedrichs iteration to convergence)"
+TTR_UNIT = "node-iterations/s"
+TTR_BYTES = 8      # algorithmic HBM bytes per node per iteration of the interior kernel: read phi, write phi
+
+
+def ttr_oracle_sample(w, target_s: float = 15.0):
+    """The oracle's Gauss-Seidel sweeps (as it stands) on the workload's domain at a coarser node count
+    sized to ~target_s seconds.  Returns (node-iterations/s, description, cores, seconds, node-iterations)."""
+    import oracle
+    from inputs import coarsened, make_v0
+    cores = oracle.max_threads()
+
+    def timed(side):
+        sub = coarsened(w, (side,) * len(w.N))
+        V0 = make_v0(sub)
+        t0 = time.perf_counter()
+        _, sweeps, _ = oracle.ttr_solve(sub.N, sub.lo, sub.hi, sub.periodic_mask, sub.dynamics, sub.params, V0,
+                                        eps=1e-6)
+        return time.perf_counter() - t0, sub, sweeps
+
+    el, sub, sweeps = timed(16)
+    side = int(16 * (target_s / max(el, 1e-3)) ** (1.0 / (len(w.N) + 1)))     # sweeps grow ~ linearly in side
+    side = max(8, min(side, max(w.N)))
+    el, sub, sweeps = timed(side)
+    work = sub.points * sweeps
+    sample = (f"oracle float64 Gauss-Seidel sweeps (Alg. 3 as printed, 8 orderings) on {w.name}'s domain at "
+              f"{'x'.join(map(str, sub.N))} nodes, to convergence (eps 1e-6): {sweeps} sweeps, {el:.1f} s, 1 thread")
+    return work / el, sample, 1, el, work
+
+
+def run_ttr(args):
+    import torch
+    from paper_2204_05520_b200 import capi
+    from inputs import TTR_CONFIGS, make_v0
+    rank, world, local = dist_env()
+    w = TTR_CONFIGS[args.config]
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    # replicas only (DESIGN.md §9): every rank solves its own copy; value = all ranks' node updates
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", init_method="env://", device_id=dev)
+    g = capi.Grid(w.N, w.lo, w.hi, w.periodic_mask)
+    V0h = make_v0(w)
+    V0 = torch.from_numpy(V0h).to(dev)
+    phi = torch.empty(w.N, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as tdist
+            tdist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch.distributed as tdist
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        capi.ttr_solve(g, w.dynamics, w.params, V0, phi=phi, stream=stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters, launches = 0, 0
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            _, info = capi.ttr_solve(g, w.dynamics, w.params, V0, phi=phi, stream=stream)
+            iters += info["iters"]
+            launches += g.launch_count()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        _, tinfo = capi.ttr_solve(g, w.dynamics, w.params, V0, phi=phi, stream=stream, use_graph=False)
+    clocks = clk.summary()
+    total_ms = max_over_ranks(e0.elapsed_time(e1))
+    value = w.points * iters * world / (total_ms / 1e3)
+    # end to end: pinned host V0 -> device -> solve -> host phi, through odp_ttr_solve_host
+    V0p = torch.from_numpy(V0h).pin_memory()
+    outp = torch.empty(w.N, dtype=torch.float32).pin_memory()
+    capi.ttr_solve_host(g, w.dynamics, w.params, V0p.numpy(), phi=outp.numpy())
+    barrier()
+    t0 = time.perf_counter()
+    e2e_it = 0
+    for _ in range(max(1, min(args.steps, 3))):
+        _, hi = capi.ttr_solve_host(g, w.dynamics, w.params, V0p.numpy(), phi=outp.numpy())
+        e2e_it += hi["iters"]
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    peak, peak_kind = measured_peaks()
+    it1 = tinfo["iters"]
+    interior_ms = tinfo["interior_ms"] / it1
+    faces_ms = tinfo["faces_ms"] / it1
+    achieved = TTR_BYTES * w.points / (interior_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(f"{w.name}:interior")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": TTR_METRIC, "value": value, "unit": TTR_UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": w.name, "grid": list(w.N), "points": w.points, "dynamics": w.dynamics,
+                   "params": list(w.params), "eps": 1e-6, "iterations_per_step": iters / args.steps,
+                   "order": "Jacobi (reading A35)",
+                   "l2": ("inputs larger than L2: 2 x %.0f MB iterates (%.0f MB) per iteration vs 126 MB L2" %
+                          (w.points * 4 / 1e6, w.points * 8 / 1e6)) if w.points * 8 > 126e6 else "iterates fit L2",
+                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas"},
+        "roofline": {"bound": "hbm", "kernel": "k_ttr_march (Alg. 3 l.5-12, interior update)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_kind": peak_kind, "bytes_per_point": TTR_BYTES,
+                     "avg_launch_ms": interior_ms, "faces_ms_per_iteration": faces_ms},
+        "clocks": clocks,
+        "e2e": {"value": w.points * e2e_it * world / e2e_s, "unit": TTR_UNIT, "h2d_bytes_per_step": w.points * 4,
+                "d2h_bytes_per_step": w.points * 4},
+        "gpu_launches": launches,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, sample, cores, el, work = ttr_oracle_sample(w, target_s=args.ref_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": TTR_UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    g.close()
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
+def run_ttr_reference(args):
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+        if rank != 0:
+            dist.barrier()
+            return
+    from inputs import TTR_CONFIGS
+    w = TTR_CONFIGS[args.config]
+    times, work = [], []
+    for i in range(args.warmup + args.steps):
+        rate, sample, cores, el, wk = ttr_oracle_sample(w, target_s=args.ref_seconds)
+        if i >= args.warmup:
+            times.append(el)
+            work.append(wk)
+    value = sum(work) / sum(times)
+    line = {"impl": "reference", "metric": TTR_METRIC, "value": value, "unit": TTR_UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "grid": list(w.N)},
+            "cpu_baseline": {"value": value, "unit": TTR_UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": TTR_UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
 
 
 def run_reference(args):
@@ -337,7 +507,10 @@ def main():
                     help="also time the single-pass variant (SURVEY.md §8(f1)) and report it beside the headline")
     ap.add_argument("--ref-seconds", type=float, default=15.0)
     args = ap.parse_args()
-    if args.impl == "reference":
+    from inputs import TTR_CONFIGS
+    if args.config in TTR_CONFIGS:
+        (run_ttr_reference if args.impl == "reference" else run_ttr)(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -200,7 +200,10 @@ typedef struct {
     int use_graph;            /* 1 -> replay chunks of iterations as a CUDA graph                */
     long long *iters_taken;   /* optional out: iterations executed                               */
     double *last_change;      /* optional out: max |phi - phi_old| of the last iteration         */
-    double *kernel_ms;        /* optional out: device time of the iteration loop                 */
+    double *kernel_ms;        /* optional out [3]: device time of the iteration loop; with
+                                 use_graph = 0 also the summed time of the interior launches [1]
+                                 and of the face launches [2] of the iterations that ran (per-launch
+                                 events), else -1                                                 */
 } odp_ttr_opts;
 
 odp_status odp_ttr_solve(odp_grid *g, int dynamics_id, const double *params, int nparams,

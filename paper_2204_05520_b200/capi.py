@@ -286,11 +286,16 @@ def _ttr_opts(eps, max_iters, big, stream_ptr, use_graph):
     o.big = float(big)
     o.stream = stream_ptr
     o.use_graph = int(bool(use_graph))
-    it, ch, km = ctypes.c_longlong(), ctypes.c_double(), ctypes.c_double()
+    it, ch, km = ctypes.c_longlong(), ctypes.c_double(), (ctypes.c_double * 3)()
     o.iters_taken = ctypes.pointer(it)
     o.last_change = ctypes.pointer(ch)
-    o.kernel_ms = ctypes.pointer(km)
+    o.kernel_ms = ctypes.cast(km, ctypes.POINTER(ctypes.c_double))
     return o, (it, ch, km)
+
+
+def _ttr_info(it, ch, km):
+    return dict(iters=it.value, last_change=ch.value, kernel_ms=km[0],
+                interior_ms=km[1] if km[1] >= 0 else None, faces_ms=km[2] if km[2] >= 0 else None)
 
 
 def ttr_solve(grid: Grid, dynamics: str, params, V0, phi=None, eps: float = 1e-6, max_iters: int = 100000,
@@ -308,7 +313,7 @@ def ttr_solve(grid: Grid, dynamics: str, params, V0, phi=None, eps: float = 1e-6
     o, (it, ch, km) = _ttr_opts(eps, max_iters, big, stream.cuda_stream, use_graph)
     _check(_lib.odp_ttr_solve(grid.handle, DYNAMICS[dynamics], pp, len(pa), V0.data_ptr(), phi.data_ptr(),
                               ctypes.byref(o)))
-    return phi, dict(iters=it.value, last_change=ch.value, kernel_ms=km.value)
+    return phi, _ttr_info(it, ch, km)
 
 
 def ttr_solve_host(grid: Grid, dynamics: str, params, V0: np.ndarray, phi=None, eps: float = 1e-6,
@@ -323,4 +328,4 @@ def ttr_solve_host(grid: Grid, dynamics: str, params, V0: np.ndarray, phi=None, 
     o, (it, ch, km) = _ttr_opts(eps, max_iters, big, None, use_graph)
     _check(_lib.odp_ttr_solve_host(grid.handle, DYNAMICS[dynamics], pp, len(pa), V0.ctypes.data, phi.ctypes.data,
                                    ctypes.byref(o)))
-    return phi, dict(iters=it.value, last_change=ch.value, kernel_ms=km.value)
+    return phi, _ttr_info(it, ch, km)

@@ -1190,15 +1190,28 @@ static odp_status ttr_device(odp_grid *g, int dyn, const double *params, int npa
     CUDA_TRY(cudaGetLastError());
     const int G = 16;                                           // iterations per chunk (even)
     const int per_iter = 1 + [&] { int c = 0; for (int d = 0; d < n; ++d) c += g->per[d] ? 0 : 1; return c; }();
+    // per-launch timing (kernel_ms with direct launches): events around the interior launch and
+    // around the face launches of every iteration
+    const bool per_launch = opts && opts->kernel_ms && !use_graph;
+    std::vector<cudaEvent_t> pev;
+    struct EvGuard { std::vector<cudaEvent_t> &v; ~EvGuard() { for (auto e : v) cudaEventDestroy(e); } } pev_guard{pev};
+    if (per_launch) {
+        pev.resize(3 * G);
+        for (auto &e : pev) CUDA_TRY(cudaEventCreate(&e));
+    }
+    double ms_interior = 0.0, ms_faces = 0.0;
     auto chunk = [&](void) -> cudaError_t {
         for (int k = 0; k < G; ++k) {
             const int par = (k + 1) & 1;
             const float *src = buf[k & 1];
             float *dst = buf[par];
+            if (per_launch) cudaEventRecord(pev[3 * k], s);
             if (fn.march) fn.march<<<grid_march, block, 0, s>>>(gd, fp, src, dst, g->d_ttr, par, last_axis < 0 ? 1 : 0, seg_len);
             else fn.rows<<<grid_rows, block, 0, s>>>(gd, fp, src, dst, g->d_ttr, par, last_axis < 0 ? 1 : 0);
+            if (per_launch) cudaEventRecord(pev[3 * k + 1], s);
             for (int d = 0; d < n; ++d)
                 if (!g->per[d]) fn.face<<<grid_face[d], block, 0, s>>>(gd, d, d == last_axis ? 1 : 0, src, dst, g->d_ttr, par);
+            if (per_launch) cudaEventRecord(pev[3 * k + 2], s);
         }
         return cudaGetLastError();
     };
@@ -1220,6 +1233,7 @@ static odp_status ttr_device(odp_grid *g, int dyn, const double *params, int npa
     CUDA_TRY(cudaEventCreate(&ev[0]));
     CUDA_TRY(cudaEventCreate(&ev[1]));
     double ms_total = 0.0;
+    long long iters_before = 0;
     odp_status rs = ODP_OK;
     for (;;) {
         cudaError_t e = cudaEventRecord(ev[0], s);
@@ -1232,6 +1246,17 @@ static odp_status ttr_device(odp_grid *g, int dyn, const double *params, int npa
         cudaEventElapsedTime(&ms, ev[0], ev[1]);
         ms_total += ms;
         g->launches += (long long)G * per_iter;
+        if (per_launch) {                    // only the iterations that ran (the rest early-exit)
+            const long long ran = g->h_ttr->iters - iters_before;
+            for (int k = 0; k < G && k < ran; ++k) {
+                float a = 0.f, b = 0.f;
+                cudaEventElapsedTime(&a, pev[3 * k], pev[3 * k + 1]);
+                cudaEventElapsedTime(&b, pev[3 * k + 1], pev[3 * k + 2]);
+                ms_interior += a;
+                ms_faces += b;
+            }
+        }
+        iters_before = g->h_ttr->iters;
         if (g->h_ttr->done) break;
     }
     if (exec) cudaGraphExecDestroy(exec);
@@ -1245,7 +1270,11 @@ static odp_status ttr_device(odp_grid *g, int dyn, const double *params, int npa
     if (opts) {
         if (opts->iters_taken) *opts->iters_taken = g->h_ttr->iters;
         if (opts->last_change) *opts->last_change = (double)__builtin_bit_cast(float, g->h_ttr->change[g->h_ttr->parity]);
-        if (opts->kernel_ms) *opts->kernel_ms = ms_total;
+        if (opts->kernel_ms) {
+            opts->kernel_ms[0] = ms_total;
+            opts->kernel_ms[1] = per_launch ? ms_interior : -1.0;
+            opts->kernel_ms[2] = per_launch ? ms_faces : -1.0;
+        }
     }
     return ODP_OK;
 }
