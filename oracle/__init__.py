@@ -64,6 +64,9 @@ def lib():
                                          ctypes.c_void_p]
         _lib.oracle_ttr_solve.argtypes = [c_int, I64, D, D, c_u32, c_int, D, c_int, F, c_dbl, c_dbl,
                                           ctypes.c_int64, D, I64, D]
+        _lib.oracle_vi_solve.argtypes = [c_int, I64, D, D, c_u32, c_int, D, c_int, F, c_dbl, ctypes.c_int64,
+                                         c_int, D, I64, D]
+        _lib.oracle_vi_successor.argtypes = [c_int, I64, D, D, c_u32, c_int, D, c_int, I64, c_int, c_int, I64]
         _lib.oracle_max_threads.restype = c_int
         _lib.oracle_cfl_dt.argtypes = [c_int, D, D, c_dbl, c_dbl]
         _lib.oracle_cfl_dt.restype = c_dbl
@@ -261,6 +264,47 @@ def ttr_solve(N, lo, hi, periodic_mask: int, dyn: str, params, V0, eps: float = 
     if st:
         raise OracleError(st)
     return out, sw.value, ch.value
+
+
+MDP_IDS = {"HOLONOMIC": 0, "DUBINS3D": 1}
+
+
+def vi_solve(N, lo, hi, periodic_mask: int, model: str, params, R, threshold: float = 1e-6,
+             max_iters: int = 100000, order: str = "jacobi"):
+    """Value iteration (Alg. 1, readings A36-A38).  R: float32 reward per node.  order "jacobi" or
+    "gauss_seidel" (in place, 8 orderings, §4.3).  Returns (V float64 of shape N, iterations, last change)."""
+    N = tuple(int(v) for v in N)
+    R = np.ascontiguousarray(R, dtype=np.float32).reshape(N)
+    Na, Np = _i64(N)
+    loa, lop = _d(lo)
+    hia, hip = _d(hi)
+    pa, pp = _d(params)
+    out = np.zeros(N, dtype=np.float64)
+    it = ctypes.c_int64()
+    ch = ctypes.c_double()
+    st = lib().oracle_vi_solve(len(N), Np, lop, hip, periodic_mask, MDP_IDS[model], pp, len(pa),
+                               R.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), float(threshold), int(max_iters),
+                               {"jacobi": 0, "gauss_seidel": 1}[order],
+                               out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(it), ctypes.byref(ch))
+    if st:
+        raise OracleError(st)
+    return out, it.value, ch.value
+
+
+def vi_successor(N, lo, hi, periodic_mask: int, model: str, params, idx, a: int, k: int) -> int:
+    """Flat index of the nearest-node successor of node idx under action a, outcome k (A36)."""
+    N = tuple(int(v) for v in N)
+    Na, Np = _i64(N)
+    loa, lop = _d(lo)
+    hia, hip = _d(hi)
+    pa, pp = _d(params)
+    ia, ip = _i64(idx)
+    out = ctypes.c_int64()
+    st = lib().oracle_vi_successor(len(N), Np, lop, hip, periodic_mask, MDP_IDS[model], pp, len(pa), ip, int(a),
+                                   int(k), ctypes.byref(out))
+    if st:
+        raise OracleError(st)
+    return out.value
 
 
 def solve_workload(w, V0=None, seed=None, **kw) -> SolveResult:

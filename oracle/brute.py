@@ -317,3 +317,105 @@ def ttr_jacobi(N, lo, hi, periodic, dyn, params, V0, eps=1e-12, max_iter=200000,
         if np.abs(phi - old).max() <= eps:
             return phi, it + 1
     return phi, max_iter
+
+
+# ------------------------------------------------------------------------------------------------
+# Value iteration (Alg. 1, readings A36-A38): an independent NumPy formulation -- successor tables
+# for every (action, outcome) at once, Jacobi iteration, and the exact Bellman fixed point by policy
+# iteration (sparse linear solves), which Alg. 1 does not use at all.
+# ------------------------------------------------------------------------------------------------
+def vi_model(model, params, n):
+    """(actions as float32 parameter rows, outcome probabilities, gamma)."""
+    f32 = np.float32
+    if model == "HOLONOMIC":
+        speed, dt, gamma = params
+        step = f32(dt) * f32(speed)
+        acts = [np.zeros(n, f32)]
+        for d in range(n):
+            for sgn in (1, -1):
+                a = np.zeros(n, f32)
+                a[d] = step if sgn > 0 else -step
+                acts.append(a)
+        return acts, np.array([1.0]), float(gamma)
+    if model == "DUBINS3D":
+        vbar, wbar, dt, slip, pslip, gamma = params
+        acts = []
+        for v in (f32(0.5) * f32(vbar), f32(vbar)):
+            for w in (-f32(wbar), f32(0.0), f32(wbar)):
+                acts.append(np.array([v, w], f32))
+        return acts, np.array([1.0 - 2.0 * pslip, pslip, pslip]), float(gamma)
+    raise ValueError(model)
+
+
+def vi_successors(N, lo, hi, periodic, model, params):
+    """succ[a][k] = flat successor index of every node (float32 arithmetic, nearest node, wrap/clamp)."""
+    f32 = np.float32
+    n = len(N)
+    dx = [(hi[d] - lo[d]) / (N[d] if periodic[d] else N[d] - 1) for d in range(n)]
+    inv_dx = [f32(1.0 / dx[d]) for d in range(n)]
+    I = np.meshgrid(*[np.arange(N[d]) for d in range(n)], indexing="ij")
+    acts, p, _ = vi_model(model, params, n)
+    K = len(p)
+    strides = [int(np.prod(N[d + 1:])) for d in range(n)]
+    out = []
+    for a in acts:
+        row = []
+        for k in range(K):
+            if model == "HOLONOMIC":
+                delta = [np.full(tuple(N), a[d], f32) for d in range(n)]
+            else:
+                th = lo[2] + I[2] * dx[2]
+                c, s = np.cos(th).astype(f32), np.sin(th).astype(f32)
+                dt = f32(params[2])
+                sig = f32(0.0) if k == 0 else (f32(params[3]) if k == 1 else -f32(params[3]))
+                dtv = dt * a[0]
+                delta = [(dtv * c) - (sig * s), (dtv * s) + (sig * c), np.full(tuple(N), dt * a[1], f32)]
+            flat = np.zeros(tuple(N), np.int64)
+            for d in range(n):
+                q = (delta[d] * inv_dx[d]).astype(f32)
+                j = I[d] + np.rint(q).astype(np.int64)
+                j = np.mod(j, N[d]) if periodic[d] else np.clip(j, 0, N[d] - 1)
+                flat = flat + j * strides[d]
+            row.append(flat.ravel())
+        out.append(row)
+    return out
+
+
+def vi_jacobi(N, lo, hi, periodic, model, params, R, iters):
+    """`iters` Jacobi iterations V_{t+1} = max_a (R + gamma sum_k p_k V_t(s'_k)) from V_0 = 0."""
+    succ = vi_successors(N, lo, hi, periodic, model, params)
+    _, p, gamma = vi_model(model, params, len(N))
+    Rf = np.asarray(R, np.float32).astype(np.float64).ravel()
+    V = np.zeros_like(Rf)
+    for _ in range(iters):
+        V = np.max([Rf + gamma * sum(p[k] * V[sa[k]] for k in range(len(p))) for sa in succ], axis=0)
+    return V.reshape(tuple(N))
+
+
+def vi_policy_iteration(N, lo, hi, periodic, model, params, R, max_rounds=200):
+    """Exact fixed point of the Bellman operator by policy iteration: evaluate the greedy policy with a
+    sparse solve of (I - gamma P_pi) V = R, improve, repeat until the policy is stable."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    succ = vi_successors(N, lo, hi, periodic, model, params)
+    _, p, gamma = vi_model(model, params, len(N))
+    Rf = np.asarray(R, np.float32).astype(np.float64).ravel()
+    P = Rf.size
+    rows = np.arange(P)
+    pol = np.zeros(P, np.int64)
+    V = np.zeros(P)
+    for _ in range(max_rounds):
+        M = sp.identity(P, format="csr")
+        for k in range(len(p)):
+            cols = np.choose(pol, [succ[a][k] for a in range(len(succ))]) if len(succ) > 1 else succ[0][k]
+            M = M - gamma * p[k] * sp.csr_matrix((np.ones(P), (rows, cols)), shape=(P, P))
+        V = spla.spsolve(M.tocsc(), Rf)
+        Q = np.array([Rf + gamma * sum(p[k] * V[sa[k]] for k in range(len(p))) for sa in succ])
+        best = Q.max(axis=0)
+        # keep the current action unless another is strictly better (ties: no change)
+        cur = Q[pol, rows]
+        new = np.where(best > cur + 1e-12 * (1 + np.abs(best)), Q.argmax(axis=0), pol)
+        if np.array_equal(new, pol):
+            return V.reshape(tuple(N))
+        pol = new
+    raise RuntimeError("policy iteration did not converge")

@@ -744,6 +744,161 @@ int oracle_ttr_solve(int n, const int64_t *N, const double *lo, const double *hi
     return OR_OK;
 }
 
+/* ------------------------------------------------------------------------------------------
+ * Continuous-MDP value iteration -- Algorithm 1 with Eq. 1-3 and the
+ * nearest-neighbour successor of the note under it.  Readings:
+ *   A36 the MDP: S = the grid's nodes; a model gives a finite action set, K outcomes per action
+ *       with probabilities p_k and displacements Delta(s, a, k); s' = the node nearest to
+ *       s + Delta: per axis i' = i + rint(Delta_d / dx_d) computed in FLOAT32 (the kernel's
+ *       precision: an integer decided by floating point), wrapped on periodic axes, clamped to
+ *       [0, N-1] on the others.  Models:
+ *         MDP_HOLONOMIC [speed, dt, gamma]: actions {stay, +-e_d}, Delta = +-dt speed e_d, K = 1.
+ *         MDP_DUBINS3D [vbar, wbar, dt, slip, pslip, gamma]: (x, y, th); actions v in {vbar/2, vbar}
+ *         x w in {-wbar, 0, wbar}; outcomes sigma in {0, +slip, -slip} with p {1-2 pslip, pslip,
+ *         pslip}; Delta = (dt v cos th - sigma sin th, dt v sin th + sigma cos th, dt w).
+ *   A37 Q(s, a) = R(s) + gamma sum_k p_k V(s'_k): Eq. 3's discount (l.6 prints no gamma; without it
+ *       the iteration diverges); the reward depends on the state only (R given per node).
+ *   A38 V_0 = 0 (l.2); one iteration takes V_{t+1}(s) = max_a Q(s, a) from V_t (l.3-7; the
+ *       max with V_{t+1}(s) initialised below every Q); stop after the first iteration with
+ *       max_s |V_{t+1}(s) - V_t(s)| < threshold (l.8-10's break read as the global test).
+ *       order 0: Jacobi (all of V_{t+1} from V_t); order 1: in place (Gauss-Seidel) with the 8
+ *       alternating orderings of §4.3 (as for Algorithm 3).  gamma < 1 makes the
+ *       Bellman operator a contraction, so both orders have the same fixed point.
+ * ---------------------------------------------------------------------------------------- */
+enum { OR_MDP_HOLONOMIC = 0, OR_MDP_DUBINS3D = 1 };
+
+typedef struct {
+    int model, n, na, K;
+    float act[12][6];        /* per action: a float32 parameter vector (model specific)          */
+    float dt, slip;
+    double p[3], gamma;
+} omdp;
+
+static int omdp_init(omdp *m, int model, int n, const double *prm, int np) {
+    memset(m, 0, sizeof(*m));
+    m->model = model; m->n = n;
+    if (model == OR_MDP_HOLONOMIC) {
+        if (np != 3 || n < 1 || n > 6) return OR_EINVAL;
+        m->na = 2 * n + 1; m->K = 1; m->p[0] = 1.0;
+        const float step = (float)prm[1] * (float)prm[0];            /* dt * speed */
+        for (int a = 1; a < m->na; ++a) {                              /* a = 1 + 2d (+), 2 + 2d (-) */
+            const int d = (a - 1) / 2;
+            m->act[a][d] = (a - 1) % 2 == 0 ? step : -step;
+        }
+        m->gamma = prm[2];
+    } else if (model == OR_MDP_DUBINS3D) {
+        if (np != 6 || n != 3) return OR_EINVAL;
+        m->na = 6; m->K = 3;
+        const float vbar = (float)prm[0], wbar = (float)prm[1];
+        for (int a = 0; a < 6; ++a) {
+            m->act[a][0] = (a / 3) == 0 ? 0.5f * vbar : vbar;          /* v */
+            m->act[a][1] = (float)(a % 3 - 1) * wbar;                   /* w in {-wbar, 0, wbar} */
+        }
+        m->dt = (float)prm[2];
+        m->slip = (float)prm[3];
+        m->p[1] = m->p[2] = prm[4];
+        m->p[0] = 1.0 - 2.0 * prm[4];
+        m->gamma = prm[5];
+    } else {
+        return OR_EINVAL;
+    }
+    if (!(m->gamma >= 0.0 && m->gamma < 1.0)) return OR_EINVAL;
+    return OR_OK;
+}
+
+/* flat index of the successor of node idx under (a, k) -- A36 (float32 decision) */
+static int64_t omdp_succ(const og *g, const omdp *m, const float *inv_dx, const int64_t *idx, int a, int k) {
+    float delta[6] = {0};
+    if (m->model == OR_MDP_HOLONOMIC) {
+        for (int d = 0; d < g->n; ++d) delta[d] = m->act[a][d];
+    } else {
+        const double th = g->x[2][idx[2]];
+        const float c = (float)cos(th), s = (float)sin(th);
+        const float sig = k == 0 ? 0.0f : (k == 1 ? m->slip : -m->slip);
+        const float dtv = m->dt * m->act[a][0];
+        const float t0 = dtv * c, t1 = sig * s, t2 = dtv * s, t3 = sig * c;
+        delta[0] = t0 - t1;
+        delta[1] = t2 + t3;
+        delta[2] = m->dt * m->act[a][1];
+    }
+    int64_t flat = 0;
+    for (int d = 0; d < g->n; ++d) {
+        const float q = delta[d] * inv_dx[d];
+        int64_t j = idx[d] + (int64_t)rintf(q);
+        if (g->per[d]) { j %= g->N[d]; if (j < 0) j += g->N[d]; }
+        else j = j < 0 ? 0 : (j > g->N[d] - 1 ? g->N[d] - 1 : j);
+        flat += j * g->stride[d];
+    }
+    return flat;
+}
+
+int oracle_vi_successor(int n, const int64_t *N, const double *lo, const double *hi, uint32_t pmask, int model,
+                        const double *prm, int np, const int64_t *idx, int a, int k, int64_t *flat_out) {
+    og g;
+    omdp m;
+    int st = og_init(&g, n, N, lo, hi, pmask);
+    if (!st) st = omdp_init(&m, model, n, prm, np);
+    if (!st && (a < 0 || a >= m.na || k < 0 || k >= m.K)) st = OR_EINVAL;
+    if (!st) {
+        float inv_dx[6];
+        for (int d = 0; d < n; ++d) inv_dx[d] = (float)(1.0 / g.dx[d]);
+        *flat_out = omdp_succ(&g, &m, inv_dx, idx, a, k);
+    }
+    og_free(&g);
+    return st;
+}
+
+int oracle_vi_solve(int n, const int64_t *N, const double *lo, const double *hi, uint32_t pmask, int model,
+                    const double *prm, int np, const float *R, double threshold, int64_t max_iters, int order,
+                    double *out, int64_t *iters_out, double *last_change) {
+    og g;
+    omdp m;
+    int st = og_init(&g, n, N, lo, hi, pmask);
+    if (st) { og_free(&g); return st; }
+    if ((st = omdp_init(&m, model, n, prm, np))) { og_free(&g); return st; }
+    if (max_iters < 1 || (order != 0 && order != 1)) { og_free(&g); return OR_EINVAL; }
+    const int64_t P = g.P;
+    float inv_dx[6];
+    for (int d = 0; d < n; ++d) inv_dx[d] = (float)(1.0 / g.dx[d]);
+    double *old = (double *)malloc(sizeof(double) * (size_t)P);
+    if (!old) { og_free(&g); return OR_ENOMEM; }
+    for (int64_t i = 0; i < P; ++i) out[i] = 0.0;                              /* l.2 */
+    int64_t it = 0;
+    double change = INFINITY;
+    while (it < max_iters) {                                                   /* l.3 */
+        memcpy(old, out, sizeof(double) * (size_t)P);
+        const double *src = order == 0 ? old : out;                           /* A38 */
+        for (int64_t kk = 0; kk < P; ++kk) {                                   /* l.4 */
+            int64_t idx[6], r = kk, flat = 0;
+            for (int d = n - 1; d >= 0; --d) {
+                int64_t i = r % g.N[d];
+                r /= g.N[d];
+                if (order == 1 && d < 3 && (((it & 7) >> d) & 1)) i = g.N[d] - 1 - i;   /* §4.3 */
+                idx[d] = i;
+            }
+            for (int d = 0; d < n; ++d) flat += idx[d] * g.stride[d];
+            double best = -INFINITY;
+            for (int a = 0; a < m.na; ++a) {                                   /* l.5 */
+                double ev = 0.0;
+                for (int k = 0; k < m.K; ++k)
+                    ev += m.p[k] * src[omdp_succ(&g, &m, inv_dx, idx, a, k)];
+                const double Q = (double)R[flat] + m.gamma * ev;                /* l.6, A37 */
+                best = fmax(best, Q);                                          /* l.7 */
+            }
+            out[flat] = best;
+        }
+        change = 0.0;
+        for (int64_t i = 0; i < P; ++i) change = fmax(change, fabs(out[i] - old[i]));   /* l.8 */
+        ++it;
+        if (change < threshold) break;                                        /* l.9-10, A38 */
+    }
+    free(old);
+    og_free(&g);
+    if (iters_out) *iters_out = it;
+    if (last_change) *last_change = change;
+    return OR_OK;
+}
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();
