@@ -213,6 +213,45 @@ odp_status odp_ttr_solve(odp_grid *g, int dynamics_id, const double *params, int
 odp_status odp_ttr_solve_host(odp_grid *g, int dynamics_id, const double *params, int nparams,
                               const float *V0, float *phi, const odp_ttr_opts *opts);
 
+/*
+ * Value iteration: Algorithm 1 for a continuous-state MDP
+ * (Eq. 1-3) discretised on the grid's nodes (readings A36-A38):
+ *     V_0 = 0;  V_{t+1}(s) = max_a [ R(s) + gamma sum_k p_k V_t(s'_k) ]
+ * until max_s |V_{t+1} - V_t| < threshold; s'_k = the node nearest to s + Delta(s, a, k), per
+ * axis i + rint(Delta_d / dx_d) in float32, wrapped on periodic axes, clamped on the others.
+ * Models (params, doubles):
+ *   ODP_MDP_HOLONOMIC [speed, dt, gamma]   any dims; actions {stay, +-e_d}, Delta = +-dt speed e_d
+ *   ODP_MDP_DUBINS3D  [vbar, wbar, dt, slip, pslip, gamma]   (x, y, th), th periodic by the caller;
+ *       actions v in {vbar/2, vbar} x w in {-wbar, 0, wbar}; outcomes sigma in {0, +slip, -slip}
+ *       with probabilities {1 - 2 pslip, pslip, pslip};
+ *       Delta = (dt v cos th - sigma sin th, dt v sin th + sigma cos th, dt w)
+ *   R  DEVICE pointer, points() floats: the reward of each node (A37)
+ *   V  DEVICE pointer, points() floats: the result (float32, Jacobi order).  Must not alias R.
+ * Errors: ODP_EINVAL (unknown model, param count, dims, gamma not in [0, 1), pslip not in
+ * [0, 0.5], partitioned handle, NULL pointers); ODP_ECUDA; ODP_ENOMEM.  Returns after the device work.
+ */
+typedef enum { ODP_MDP_HOLONOMIC = 0, ODP_MDP_DUBINS3D = 1 } odp_mdp_model;
+
+typedef struct {
+    double threshold;         /* stop after the first iteration with change < threshold; <= 0 -> 1e-6 */
+    long long max_iters;      /* <= 0 -> 100000                                                  */
+    int fixed_iters;          /* 1 -> ignore the threshold: run exactly max_iters iterations      */
+    void *stream;             /* cudaStream_t; NULL -> the library's own stream                  */
+    int use_graph;            /* 1 -> replay chunks of iterations as a CUDA graph                */
+    long long *iters_taken;   /* optional out: iterations executed                               */
+    double *last_change;      /* optional out: max |V_{t+1} - V_t| of the last iteration          */
+    double *kernel_ms;        /* optional out [2]: device time of the iteration loop; with
+                                 use_graph = 0 also the summed time of the iteration launches [1],
+                                 else -1                                                          */
+} odp_vi_opts;
+
+odp_status odp_vi_solve(odp_grid *g, int model_id, const double *params, int nparams,
+                        const float *R, float *V, const odp_vi_opts *opts);
+
+/* As odp_vi_solve with HOST R and V (copies inside the call). */
+odp_status odp_vi_solve_host(odp_grid *g, int model_id, const double *params, int nparams,
+                             const float *R, float *V, const odp_vi_opts *opts);
+
 /* Number of kernel launches issued by the last solve on this handle (launch accounting). */
 long long odp_last_launch_count(const odp_grid *g);
 

@@ -117,6 +117,62 @@ T1 = Workload(
 TTR_CONFIGS = {T1.name: T1}
 
 
+# value iteration (Algorithm 1) workloads.  Table 3 times
+# value iteration on 3D grids 25x25x9, 40x40x20, 50x50x30 without stating the MDP; reading A36's
+# Dubins-car MDP stands in: x, y in [-5, 5], th in [-pi, pi) periodic, v in {0.5, 1}, |w| <= 1,
+# dt = 0.25, lateral slip 0.1 with probability 0.1 each side, gamma = 0.95; reward +1 on a goal disc
+# (centre (3, 2), radius 1), -1 on an obstacle disc (centre (-1, 0), radius 1.5), 0 elsewhere.
+@dataclass(frozen=True)
+class MdpWorkload:
+    name: str
+    N: Tuple[int, ...]
+    lo: Tuple[float, ...]
+    hi: Tuple[float, ...]
+    periodic: Tuple[int, ...]
+    model: str
+    params: Tuple[float, ...]
+    goal: Tuple[float, float, float]
+    obstacle: Tuple[float, float, float]
+    note: str = ""
+
+    @property
+    def points(self) -> int:
+        return int(np.prod(self.N, dtype=np.int64))
+
+    @property
+    def periodic_mask(self) -> int:
+        return sum(1 << d for d, p in enumerate(self.periodic) if p)
+
+
+def _vi(name, N, note=""):
+    return MdpWorkload(name=name, N=N, lo=(-5.0, -5.0, -PI), hi=(5.0, 5.0, PI), periodic=(0, 0, 1),
+                       model="DUBINS3D", params=(1.0, 1.0, 0.25, 0.1, 0.1, 0.95), goal=(3.0, 2.0, 1.0),
+                       obstacle=(-1.0, 0.0, 1.5), note=note)
+
+
+VI_CONFIGS = {w.name: w for w in (
+    _vi("v0", (25, 25, 9), "Table 3 smallest shape"),
+    _vi("v1", (50, 50, 30), "Table 3 largest shape"),
+    _vi("v2", (384, 384, 128), "the same MDP at 1.9e7 nodes (3 float32 arrays = 226 MB, above L2)"),
+)}
+
+
+def make_reward(w: MdpWorkload, seed: Optional[int] = None, noise: float = 1e-3) -> np.ndarray:
+    """Reward per node (float32): +1 on the goal disc, -1 on the obstacle disc (x, y only), 0 else;
+    seed adds noise * U(-1, 1)."""
+    ax = [axis_nodes(n, l, h, bool(p)) for n, l, h, p in zip(w.N, w.lo, w.hi, w.periodic)]
+    X, Y = np.meshgrid(ax[0], ax[1], indexing="ij")
+    R2 = np.zeros(X.shape)
+    gx, gy, gr = w.goal
+    ox, oy, orad = w.obstacle
+    R2[(X - gx) ** 2 + (Y - gy) ** 2 <= gr ** 2] = 1.0
+    R2[(X - ox) ** 2 + (Y - oy) ** 2 <= orad ** 2] = -1.0
+    R = np.broadcast_to(R2[..., None], w.N).astype(np.float64)
+    if seed is not None:
+        R = R + noise * np.random.default_rng(seed).uniform(-1.0, 1.0, w.N)
+    return np.ascontiguousarray(R.astype(np.float32))
+
+
 def axis_nodes(N: int, lo: float, hi: float, periodic: bool) -> np.ndarray:
     """Node positions of one axis (problem statement; reading A15)."""
     h = (hi - lo) / (N if periodic else (N - 1))

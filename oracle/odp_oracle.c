@@ -769,7 +769,7 @@ enum { OR_MDP_HOLONOMIC = 0, OR_MDP_DUBINS3D = 1 };
 
 typedef struct {
     int model, n, na, K;
-    float act[12][6];        /* per action: a float32 parameter vector (model specific)          */
+    float act[13][6];        /* per action (at most 2n + 1 = 13): float32 parameters of the model */
     float dt, slip;
     double p[3], gamma;
 } omdp;

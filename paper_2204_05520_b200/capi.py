@@ -24,7 +24,9 @@ DYNAMICS = {"HOLONOMIC_BALL": 0, "HOLONOMIC_BOX": 1, "DUBINS3D": 2, "CAR4D": 3, 
 # every symbol include/odp.h declares (checked by tests/test_capi_host.py)
 EXPORTS = ("odp_grid_create", "odp_grid_destroy", "odp_grid_info", "odp_hj_solve", "odp_hj_solve_host",
            "odp_partition_extent", "odp_comm_unique_id", "odp_grid_partition", "odp_grid_local_extent",
-           "odp_last_launch_count", "odp_last_error", "odp_version", "odp_ttr_solve", "odp_ttr_solve_host")
+           "odp_last_launch_count", "odp_last_error", "odp_version", "odp_ttr_solve", "odp_ttr_solve_host",
+           "odp_vi_solve", "odp_vi_solve_host")
+MDP_MODELS = {"HOLONOMIC": 0, "DUBINS3D": 1}
 
 
 class odp_solve_opts(ctypes.Structure):
@@ -46,6 +48,17 @@ class odp_ttr_opts(ctypes.Structure):
     _fields_ = [("eps", ctypes.c_double),
                 ("max_iters", ctypes.c_longlong),
                 ("big", ctypes.c_double),
+                ("stream", ctypes.c_void_p),
+                ("use_graph", ctypes.c_int),
+                ("iters_taken", ctypes.POINTER(ctypes.c_longlong)),
+                ("last_change", ctypes.POINTER(ctypes.c_double)),
+                ("kernel_ms", ctypes.POINTER(ctypes.c_double))]
+
+
+class odp_vi_opts(ctypes.Structure):
+    _fields_ = [("threshold", ctypes.c_double),
+                ("max_iters", ctypes.c_longlong),
+                ("fixed_iters", ctypes.c_int),
                 ("stream", ctypes.c_void_p),
                 ("use_graph", ctypes.c_int),
                 ("iters_taken", ctypes.POINTER(ctypes.c_longlong)),
@@ -81,6 +94,10 @@ def _load():
     for name in ("odp_ttr_solve", "odp_ttr_solve_host"):
         f = getattr(lib, name)
         f.argtypes = [vp, ctypes.c_int, D, ctypes.c_int, vp, vp, ctypes.POINTER(odp_ttr_opts)]
+        f.restype = ctypes.c_int
+    for name in ("odp_vi_solve", "odp_vi_solve_host"):
+        f = getattr(lib, name)
+        f.argtypes = [vp, ctypes.c_int, D, ctypes.c_int, vp, vp, ctypes.POINTER(odp_vi_opts)]
         f.restype = ctypes.c_int
     lib.odp_partition_extent.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, I64, I64]
     lib.odp_partition_extent.restype = ctypes.c_int
@@ -329,3 +346,52 @@ def ttr_solve_host(grid: Grid, dynamics: str, params, V0: np.ndarray, phi=None, 
     _check(_lib.odp_ttr_solve_host(grid.handle, DYNAMICS[dynamics], pp, len(pa), V0.ctypes.data, phi.ctypes.data,
                                    ctypes.byref(o)))
     return phi, _ttr_info(it, ch, km)
+
+
+def _vi_opts(threshold, max_iters, fixed_iters, stream_ptr, use_graph):
+    o = odp_vi_opts()
+    o.threshold = float(threshold)
+    o.max_iters = int(max_iters)
+    o.fixed_iters = int(bool(fixed_iters))
+    o.stream = stream_ptr
+    o.use_graph = int(bool(use_graph))
+    it, ch, km = ctypes.c_longlong(), ctypes.c_double(), (ctypes.c_double * 2)()
+    o.iters_taken = ctypes.pointer(it)
+    o.last_change = ctypes.pointer(ch)
+    o.kernel_ms = ctypes.cast(km, ctypes.POINTER(ctypes.c_double))
+    return o, (it, ch, km)
+
+
+def _vi_info(it, ch, km):
+    return dict(iters=it.value, last_change=ch.value, kernel_ms=km[0], iter_ms=km[1] if km[1] >= 0 else None)
+
+
+def vi_solve(grid: Grid, model: str, params, R, V=None, threshold: float = 1e-6, max_iters: int = 100000,
+             fixed_iters: bool = False, stream=None, use_graph: bool = True):
+    """odp_vi_solve (Algorithm 1) on torch CUDA tensors.  Returns (V, info)."""
+    import torch
+    assert R.is_cuda and R.dtype == torch.float32 and R.is_contiguous() and R.numel() == grid.points
+    if V is None:
+        V = torch.empty(tuple(grid.local_N), dtype=torch.float32, device=R.device)
+    assert V.is_cuda and V.dtype == torch.float32 and V.is_contiguous() and V.numel() == grid.points
+    if stream is None:
+        stream = torch.cuda.current_stream(R.device)
+    pa, pp = _dp(params)
+    o, keep = _vi_opts(threshold, max_iters, fixed_iters, stream.cuda_stream, use_graph)
+    _check(_lib.odp_vi_solve(grid.handle, MDP_MODELS[model], pp, len(pa), R.data_ptr(), V.data_ptr(), ctypes.byref(o)))
+    return V, _vi_info(*keep)
+
+
+def vi_solve_host(grid: Grid, model: str, params, R: np.ndarray, V=None, threshold: float = 1e-6,
+                  max_iters: int = 100000, fixed_iters: bool = False, use_graph: bool = True):
+    """odp_vi_solve_host: R / V are host float32 arrays (copies inside the call)."""
+    R = np.ascontiguousarray(R, dtype=np.float32)
+    assert R.size == grid.points
+    if V is None:
+        V = np.empty(tuple(grid.local_N), dtype=np.float32)
+    assert V.dtype == np.float32 and V.flags["C_CONTIGUOUS"] and V.size == grid.points
+    pa, pp = _dp(params)
+    o, keep = _vi_opts(threshold, max_iters, fixed_iters, None, use_graph)
+    _check(_lib.odp_vi_solve_host(grid.handle, MDP_MODELS[model], pp, len(pa), R.ctypes.data, V.ctypes.data,
+                                  ctypes.byref(o)))
+    return V, _vi_info(*keep)

@@ -32,7 +32,9 @@ struct TtrState {
     long long iters;      // iterations executed
     long long max_iters;
     float eps;
-    unsigned blocks_done; // CTAs of the current k_ttr_faces launch that finished
+    unsigned blocks_done; // CTAs of the iteration's last launch that finished
+    int strict;           // stop on change < eps (value iteration, A38) instead of <= eps (A31)
+    int pad;
 };
 
 __device__ __forceinline__ bool is_target(float v) { return __float_as_uint(v) == 0x80000000u; }
@@ -50,14 +52,15 @@ __device__ __forceinline__ void ttr_last_cta_control(TtrState *st, int par) {
     __shared__ bool last;
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(&st->blocks_done, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) last = atomicAdd(&st->blocks_done, 1u) == gridDim.x * gridDim.y * gridDim.z - 1;
     __syncthreads();
     if (last && threadIdx.x == 0) {
         __threadfence();
         st->blocks_done = 0u;
         st->iters += 1;
         const float c = __uint_as_float(atomicAdd(&st->change[par], 0u));
-        if (c <= st->eps || st->iters >= st->max_iters) { st->done = 1; st->parity = par; }
+        const bool conv = st->strict ? c < st->eps : c <= st->eps;
+        if (conv || st->iters >= st->max_iters) { st->done = 1; st->parity = par; }
         else st->change[par ^ 1] = 0u;
     }
 }
@@ -75,8 +78,9 @@ __global__ void __launch_bounds__(256) k_ttr_finish(long long P, const float *sr
         phi[i] = fabsf(src[i]);                                           // -0 target marker -> 0
 }
 
-__global__ void k_ttr_reset(TtrState *st, long long max_iters, float eps) {
+__global__ void k_ttr_reset(TtrState *st, long long max_iters, float eps, int strict) {
     st->change[0] = st->change[1] = 0u;
+    st->strict = strict;
     st->done = 0; st->parity = 0; st->iters = 0;
     st->max_iters = max_iters; st->eps = eps;
     st->blocks_done = 0u;

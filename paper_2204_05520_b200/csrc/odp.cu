@@ -20,6 +20,7 @@
 #include "../../include/odp.h"
 #include "kernels_march.cuh"
 #include "kernels_ttr.cuh"
+#include "kernels_vi.cuh"
 
 using namespace odp;
 
@@ -1133,6 +1134,77 @@ static TtrFns ttr_select(int dyn, int n) {
     }
 }
 
+// ------------------------------------------------------------------------------------------------
+// iterate-to-convergence driver shared by time-to-reach (Alg. 3) and value iteration (Alg. 1):
+// chunks of G iterations (direct launches or one CUDA graph per chunk), each iteration's launches
+// early-exit once the device state says done; the host reads the 40-byte TtrState per chunk.
+// launch_iter(k, ev) launches iteration k of a chunk (k even: buffer 0 -> 1), recording ev[0..2]
+// around its two launch groups when ev is non-null (per-launch timing, direct launches only).
+// ------------------------------------------------------------------------------------------------
+static odp_status iterate_to_convergence(odp_grid *g, cudaStream_t s, int per_iter, bool use_graph, bool per_launch,
+                                         const std::function<void(int, const cudaEvent_t *)> &launch_iter,
+                                         double *ms_total, double *ms_a, double *ms_b) {
+    const int G = 16;                                           // iterations per chunk (even)
+    std::vector<cudaEvent_t> pev;
+    struct EvGuard { std::vector<cudaEvent_t> &v; ~EvGuard() { for (auto e : v) cudaEventDestroy(e); } } pev_guard{pev};
+    if (per_launch) {
+        pev.resize(3 * G);
+        for (auto &e : pev) CUDA_TRY(cudaEventCreate(&e));
+    }
+    auto chunk = [&](void) -> cudaError_t {
+        for (int k = 0; k < G; ++k) launch_iter(k, per_launch ? &pev[3 * k] : nullptr);
+        return cudaGetLastError();
+    };
+    cudaGraphExec_t exec = nullptr;
+    if (use_graph) {
+        cudaGraph_t graph = nullptr;
+        CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        cudaError_t e = chunk();
+        cudaError_t e2 = cudaStreamEndCapture(s, &graph);
+        if (e != cudaSuccess || e2 != cudaSuccess) {
+            if (graph) cudaGraphDestroy(graph);
+            return fail(ODP_ECUDA, "graph capture: %s", cudaGetErrorString(e != cudaSuccess ? e : e2));
+        }
+        e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return fail(ODP_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    }
+    cudaEvent_t ev[2];
+    CUDA_TRY(cudaEventCreate(&ev[0]));
+    CUDA_TRY(cudaEventCreate(&ev[1]));
+    *ms_total = 0.0; *ms_a = 0.0; *ms_b = 0.0;
+    long long iters_before = 0;
+    odp_status rs = ODP_OK;
+    for (;;) {
+        cudaError_t e = cudaEventRecord(ev[0], s);
+        if (e == cudaSuccess) e = use_graph ? cudaGraphLaunch(exec, s) : chunk();
+        if (e == cudaSuccess) e = cudaEventRecord(ev[1], s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(g->h_ttr, g->d_ttr, sizeof(TtrState), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) { rs = fail(ODP_ECUDA, "iteration: %s", cudaGetErrorString(e)); break; }
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[0], ev[1]);
+        *ms_total += ms;
+        g->launches += (long long)G * per_iter;
+        if (per_launch) {                    // only the iterations that ran (the rest early-exit)
+            const long long ran = g->h_ttr->iters - iters_before;
+            for (int k = 0; k < G && k < ran; ++k) {
+                float a = 0.f, b = 0.f;
+                cudaEventElapsedTime(&a, pev[3 * k], pev[3 * k + 1]);
+                cudaEventElapsedTime(&b, pev[3 * k + 1], pev[3 * k + 2]);
+                *ms_a += a;
+                *ms_b += b;
+            }
+        }
+        iters_before = g->h_ttr->iters;
+        if (g->h_ttr->done) break;
+    }
+    if (exec) cudaGraphExecDestroy(exec);
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    return rs;
+}
+
 static odp_status ttr_device(odp_grid *g, int dyn, const double *params, int nparams, const float *V0, float *phi,
                              const odp_ttr_opts *opts) {
     odp_status st = validate_dyn(g, dyn, params, nparams);
@@ -1184,85 +1256,26 @@ static odp_status ttr_device(odp_grid *g, int dyn, const double *params, int npa
     float *buf[2] = {phi, g->d_buf[0] + g->halo_elems};
     g->launches = 0;
 
-    k_ttr_reset<<<1, 1, 0, s>>>(g->d_ttr, max_iters, (float)eps);
+    k_ttr_reset<<<1, 1, 0, s>>>(g->d_ttr, max_iters, (float)eps, 0);
     k_ttr_init<<<grid_all, block, 0, s>>>(P, V0, (float)big, buf[0]);
     g->launches += 2;
     CUDA_TRY(cudaGetLastError());
-    const int G = 16;                                           // iterations per chunk (even)
     const int per_iter = 1 + [&] { int c = 0; for (int d = 0; d < n; ++d) c += g->per[d] ? 0 : 1; return c; }();
-    // per-launch timing (kernel_ms with direct launches): events around the interior launch and
-    // around the face launches of every iteration
     const bool per_launch = opts && opts->kernel_ms && !use_graph;
-    std::vector<cudaEvent_t> pev;
-    struct EvGuard { std::vector<cudaEvent_t> &v; ~EvGuard() { for (auto e : v) cudaEventDestroy(e); } } pev_guard{pev};
-    if (per_launch) {
-        pev.resize(3 * G);
-        for (auto &e : pev) CUDA_TRY(cudaEventCreate(&e));
-    }
-    double ms_interior = 0.0, ms_faces = 0.0;
-    auto chunk = [&](void) -> cudaError_t {
-        for (int k = 0; k < G; ++k) {
-            const int par = (k + 1) & 1;
-            const float *src = buf[k & 1];
-            float *dst = buf[par];
-            if (per_launch) cudaEventRecord(pev[3 * k], s);
-            if (fn.march) fn.march<<<grid_march, block, 0, s>>>(gd, fp, src, dst, g->d_ttr, par, last_axis < 0 ? 1 : 0, seg_len);
-            else fn.rows<<<grid_rows, block, 0, s>>>(gd, fp, src, dst, g->d_ttr, par, last_axis < 0 ? 1 : 0);
-            if (per_launch) cudaEventRecord(pev[3 * k + 1], s);
-            for (int d = 0; d < n; ++d)
-                if (!g->per[d]) fn.face<<<grid_face[d], block, 0, s>>>(gd, d, d == last_axis ? 1 : 0, src, dst, g->d_ttr, par);
-            if (per_launch) cudaEventRecord(pev[3 * k + 2], s);
-        }
-        return cudaGetLastError();
-    };
-    cudaGraphExec_t exec = nullptr;
-    if (use_graph) {
-        cudaGraph_t graph = nullptr;
-        CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        cudaError_t e = chunk();
-        cudaError_t e2 = cudaStreamEndCapture(s, &graph);
-        if (e != cudaSuccess || e2 != cudaSuccess) {
-            if (graph) cudaGraphDestroy(graph);
-            return fail(ODP_ECUDA, "graph capture: %s", cudaGetErrorString(e != cudaSuccess ? e : e2));
-        }
-        e = cudaGraphInstantiate(&exec, graph, 0);
-        cudaGraphDestroy(graph);
-        if (e != cudaSuccess) return fail(ODP_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
-    }
-    cudaEvent_t ev[2];
-    CUDA_TRY(cudaEventCreate(&ev[0]));
-    CUDA_TRY(cudaEventCreate(&ev[1]));
-    double ms_total = 0.0;
-    long long iters_before = 0;
-    odp_status rs = ODP_OK;
-    for (;;) {
-        cudaError_t e = cudaEventRecord(ev[0], s);
-        if (e == cudaSuccess) e = use_graph ? cudaGraphLaunch(exec, s) : chunk();
-        if (e == cudaSuccess) e = cudaEventRecord(ev[1], s);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(g->h_ttr, g->d_ttr, sizeof(TtrState), cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        if (e != cudaSuccess) { rs = fail(ODP_ECUDA, "ttr iteration: %s", cudaGetErrorString(e)); break; }
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, ev[0], ev[1]);
-        ms_total += ms;
-        g->launches += (long long)G * per_iter;
-        if (per_launch) {                    // only the iterations that ran (the rest early-exit)
-            const long long ran = g->h_ttr->iters - iters_before;
-            for (int k = 0; k < G && k < ran; ++k) {
-                float a = 0.f, b = 0.f;
-                cudaEventElapsedTime(&a, pev[3 * k], pev[3 * k + 1]);
-                cudaEventElapsedTime(&b, pev[3 * k + 1], pev[3 * k + 2]);
-                ms_interior += a;
-                ms_faces += b;
-            }
-        }
-        iters_before = g->h_ttr->iters;
-        if (g->h_ttr->done) break;
-    }
-    if (exec) cudaGraphExecDestroy(exec);
-    cudaEventDestroy(ev[0]);
-    cudaEventDestroy(ev[1]);
-    if (rs) return rs;
+    double ms_total = 0.0, ms_interior = 0.0, ms_faces = 0.0;
+    st = iterate_to_convergence(g, s, per_iter, use_graph, per_launch, [&](int k, const cudaEvent_t *ev) {
+        const int par = (k + 1) & 1;
+        const float *src = buf[k & 1];
+        float *dst = buf[par];
+        if (ev) cudaEventRecord(ev[0], s);
+        if (fn.march) fn.march<<<grid_march, block, 0, s>>>(gd, fp, src, dst, g->d_ttr, par, last_axis < 0 ? 1 : 0, seg_len);
+        else fn.rows<<<grid_rows, block, 0, s>>>(gd, fp, src, dst, g->d_ttr, par, last_axis < 0 ? 1 : 0);
+        if (ev) cudaEventRecord(ev[1], s);
+        for (int d = 0; d < n; ++d)
+            if (!g->per[d]) fn.face<<<grid_face[d], block, 0, s>>>(gd, d, d == last_axis ? 1 : 0, src, dst, g->d_ttr, par);
+        if (ev) cudaEventRecord(ev[2], s);
+    }, &ms_total, &ms_interior, &ms_faces);
+    if (st) return st;
     k_ttr_finish<<<grid_all, block, 0, s>>>(P, buf[g->h_ttr->parity], phi);
     g->launches += 1;
     CUDA_TRY(cudaGetLastError());
@@ -1310,6 +1323,122 @@ extern "C" odp_status odp_ttr_solve_host(odp_grid *g, int dynamics_id, const dou
     }
     cudaFreeAsync(dV0, s);
     cudaFreeAsync(dphi, s);
+    cudaStreamSynchronize(s);
+    return st;
+}
+
+// ------------------------------------------------------------------------------------------------
+// value iteration (Algorithm 1; readings A36-A38)
+// ------------------------------------------------------------------------------------------------
+static odp_status vi_device(odp_grid *g, int model, const double *params, int nparams, const float *R, float *V,
+                            const odp_vi_opts *opts) {
+    if (!g) return fail(ODP_EINVAL, "NULL grid");
+    if (model != ODP_MDP_HOLONOMIC && model != ODP_MDP_DUBINS3D) return fail(ODP_EINVAL, "unknown MDP model %d", model);
+    const int want = model == ODP_MDP_HOLONOMIC ? 3 : 6;
+    if (!params || nparams != want) return fail(ODP_EINVAL, "MDP model %d takes %d params (got %d)", model, want, nparams);
+    for (int k = 0; k < nparams; ++k) if (!std::isfinite(params[k])) return fail(ODP_EINVAL, "param %d not finite", k);
+    if (model == ODP_MDP_DUBINS3D && g->n != 3) return fail(ODP_EINVAL, "MDP model 1 needs dims=3 (grid has %d)", g->n);
+    const double gamma = params[nparams - 1];
+    if (!(gamma >= 0.0 && gamma < 1.0)) return fail(ODP_EINVAL, "gamma must be in [0, 1)");
+    if (model == ODP_MDP_DUBINS3D && !(params[4] >= 0.0 && params[4] <= 0.5)) return fail(ODP_EINVAL, "pslip must be in [0, 0.5]");
+    if (!R || !V) return fail(ODP_EINVAL, "NULL R/V");
+    if (R == V) return fail(ODP_EINVAL, "V aliases R");
+    if (g->nranks > 1 || g->comm) return fail(ODP_EINVAL, "value iteration runs on an unpartitioned grid");
+    const double thr = (opts && opts->threshold > 0.0) ? opts->threshold : 1e-6;
+    const long long max_iters = (opts && opts->max_iters > 0) ? opts->max_iters : 100000;
+    const bool fixed = opts && opts->fixed_iters;
+    const bool use_graph = opts ? opts->use_graph != 0 : true;
+    odp_status st;
+    if ((st = ensure_device(g, 1))) return st;
+    if (!g->d_ttr) {
+        CUDA_TRY(cudaMalloc(&g->d_ttr, sizeof(TtrState)));
+        CUDA_TRY(cudaMallocHost(&g->h_ttr, sizeof(TtrState)));
+    }
+    cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
+    MdpParams mp;
+    memset(&mp, 0, sizeof mp);
+    if (model == ODP_MDP_HOLONOMIC) {
+        mp.step = (float)params[1] * (float)params[0];
+        mp.p[0] = 1.f;
+    } else {
+        mp.vbar = (float)params[0]; mp.wbar = (float)params[1]; mp.dt = (float)params[2]; mp.slip = (float)params[3];
+        mp.p[0] = (float)(1.0 - 2.0 * params[4]); mp.p[1] = mp.p[2] = (float)params[4];
+    }
+    mp.gamma = (float)gamma;
+    const vi_march_fn fn = vi_select(model, g->n);
+    GridDev gd = make_griddev(g);
+    int nsm = 148, dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int block = 256;
+    const long long P = local_points(g);
+    const long long ncol = P / g->n0;
+    const int col_blocks = (int)((ncol + block - 1) / block);
+    int nseg = (int)std::max<long long>(1, std::min<long long>(g->n0, ((long long)nsm * 8 + col_blocks - 1) / col_blocks));
+    const int seg_len = (int)((g->n0 + nseg - 1) / nseg);
+    nseg = (int)((g->n0 + seg_len - 1) / seg_len);
+    const dim3 grid_march(col_blocks, nseg);
+    float *buf[2] = {V, g->d_buf[0] + g->halo_elems};
+    g->launches = 0;
+    k_ttr_reset<<<1, 1, 0, s>>>(g->d_ttr, max_iters, fixed ? -1.f : (float)thr, 1);
+    CUDA_TRY(cudaMemsetAsync(buf[0], 0, (size_t)P * sizeof(float), s));           // l.2: V_0 = 0
+    g->launches += 1;
+    CUDA_TRY(cudaGetLastError());
+    const bool per_launch = opts && opts->kernel_ms && !use_graph;
+    double ms_total = 0.0, ms_iter = 0.0, ms_unused = 0.0;
+    st = iterate_to_convergence(g, s, 1, use_graph, per_launch, [&](int k, const cudaEvent_t *ev) {
+        const int par = (k + 1) & 1;
+        if (ev) cudaEventRecord(ev[0], s);
+        fn<<<grid_march, block, 0, s>>>(gd, mp, R, buf[k & 1], buf[par], g->d_ttr, par, seg_len);
+        if (ev) { cudaEventRecord(ev[1], s); cudaEventRecord(ev[2], s); }
+    }, &ms_total, &ms_iter, &ms_unused);
+    if (st) return st;
+    if (g->h_ttr->parity == 1) {
+        CUDA_TRY(cudaMemcpyAsync(V, buf[1], (size_t)P * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    }
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (opts) {
+        if (opts->iters_taken) *opts->iters_taken = g->h_ttr->iters;
+        if (opts->last_change) *opts->last_change = (double)__builtin_bit_cast(float, g->h_ttr->change[g->h_ttr->parity]);
+        if (opts->kernel_ms) {
+            opts->kernel_ms[0] = ms_total;
+            opts->kernel_ms[1] = per_launch ? ms_iter : -1.0;
+        }
+    }
+    return ODP_OK;
+}
+
+extern "C" odp_status odp_vi_solve(odp_grid *g, int model_id, const double *params, int nparams, const float *R,
+                                   float *V, const odp_vi_opts *opts) {
+    g_err.clear();
+    return vi_device(g, model_id, params, nparams, R, V, opts);
+}
+
+extern "C" odp_status odp_vi_solve_host(odp_grid *g, int model_id, const double *params, int nparams,
+                                        const float *R, float *V, const odp_vi_opts *opts) {
+    g_err.clear();
+    if (!g) return fail(ODP_EINVAL, "NULL grid");
+    if (!R || !V) return fail(ODP_EINVAL, "NULL R/V");
+    odp_status st;
+    if ((st = ensure_device(g, 1))) return st;
+    const size_t bytes = (size_t)local_points(g) * sizeof(float);
+    cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
+    float *dR = nullptr, *dV = nullptr;
+    CUDA_TRY(cudaMallocAsync(&dR, bytes, s));
+    CUDA_TRY(cudaMallocAsync(&dV, bytes, s));
+    odp_vi_opts o;
+    memset(&o, 0, sizeof o);
+    if (opts) o = *opts; else o.use_graph = 1;
+    o.stream = s;
+    CUDA_TRY(cudaMemcpyAsync(dR, R, bytes, cudaMemcpyHostToDevice, s));
+    st = vi_device(g, model_id, params, nparams, dR, dV, &o);
+    if (st == ODP_OK) {
+        cudaError_t e = cudaMemcpyAsync(V, dV, bytes, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = fail(ODP_ECUDA, "copy out: %s", cudaGetErrorString(e));
+    }
+    cudaFreeAsync(dR, s);
+    cudaFreeAsync(dV, s);
     cudaStreamSynchronize(s);
     return st;
 }

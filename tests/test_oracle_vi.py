@@ -118,3 +118,16 @@ def test_vi_jacobi_iterates_equal_numpy():
     for t in (1, 3, 8):
         V, it, _ = oracle.vi_solve(N, lo, hi, 4, "DUBINS3D", prm, R, threshold=0.0, max_iters=t)
         np.testing.assert_allclose(V, brute.vi_jacobi(N, lo, hi, (0, 0, 1), "DUBINS3D", prm, R, t), atol=1e-13)
+
+
+@pytest.mark.parametrize("N,per", [((5, 6, 5, 4, 6, 5), (0,) * 6), ((9, 10, 11, 7), (0, 1, 0, 1)), ((13,), (1,))])
+def test_vi_holonomic_jacobi_iterates_equal_numpy(N, per):
+    n = len(N)
+    lo = tuple(-5.0 + d for d in range(n))
+    hi = tuple(5.0 + 0.5 * d for d in range(n))
+    R = np.random.default_rng(1).uniform(-1, 1, N).astype(np.float32)
+    prm = (2.0, 0.9, 0.8)       # step 1.8: shifts of 0..2 cells depending on the axis spacing
+    pm = sum(1 << d for d in range(n) if per[d])
+    for t in (1, 4):
+        V, _, _ = oracle.vi_solve(N, lo, hi, pm, "HOLONOMIC", prm, R, threshold=0.0, max_iters=t)
+        np.testing.assert_allclose(V, brute.vi_jacobi(N, lo, hi, per, "HOLONOMIC", prm, R, t), atol=1e-13)
