@@ -11,6 +11,8 @@ the largest config that fits one GPU and the one BASELINE.json's scaling target 
 
 --config t1 measures SURVEY.md §8(f3) instead: time-to-reach (Algorithm 3) on the Dubins car at 256^3,
 a step = one odp_ttr_solve to convergence, value = node updates (nodes x iterations) / device time.
+--config v2 (v0, v1) measures SURVEY.md §8(f4): value iteration (Algorithm 1) on the Dubins-car MDP,
+a step = one odp_vi_solve to convergence; the line also carries Table 3's grid shapes in seconds.
 """
 from __future__ import annotations
 
@@ -313,6 +315,183 @@ def run_ttr_reference(args):
         dist.barrier()
 
 
+# --------------------------------------------------------------------------------------------------
+# value iteration (Algorithm 1) -- a step is one odp_vi_solve to convergence
+# --------------------------------------------------------------------------------------------------
+VI_METRIC = "value-iteration node updates/s (Bellman iterations to convergence)"
+VI_UNIT = "node-iterations/s"
+VI_BYTES = 12      # algorithmic HBM bytes per node per iteration: read R, read V_t (gathers hit L1/L2), write V_t+1
+
+
+def vi_oracle_sample(w, target_s: float = 15.0):
+    """The oracle's Jacobi value iteration (as it stands, 1 thread) on the workload's domain at a
+    node count sized to ~target_s seconds, to the same threshold."""
+    import oracle
+    from inputs import make_reward
+    from dataclasses import replace
+
+    def timed(scale):
+        N = tuple(max(4, int(round(n * scale))) for n in w.N)
+        sub = replace(w, N=N)
+        R = make_reward(sub)
+        t0 = time.perf_counter()
+        _, it, _ = oracle.vi_solve(sub.N, sub.lo, sub.hi, sub.periodic_mask, sub.model, sub.params, R, threshold=1e-6)
+        return time.perf_counter() - t0, sub, it
+
+    el, sub, it = timed(min(1.0, 20.0 / max(w.N)))
+    scale = min(1.0, 20.0 / max(w.N)) * (target_s / max(el, 1e-3)) ** (1.0 / 3.0)
+    el, sub, it = timed(min(1.0, scale))
+    work = sub.points * it
+    sample = (f"oracle float64 Jacobi value iteration (Alg. 1, 1 thread) on {w.name}'s MDP at "
+              f"{'x'.join(map(str, sub.N))} nodes to threshold 1e-6: {it} iterations, {el:.1f} s")
+    return work / el, sample, 1, el, work
+
+
+def run_vi(args):
+    import torch
+    from paper_2204_05520_b200 import capi
+    from inputs import VI_CONFIGS, make_reward
+    rank, world, local = dist_env()
+    w = VI_CONFIGS[args.config]
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:                                  # replicas only (DESIGN.md §9)
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", init_method="env://", device_id=dev)
+    g = capi.Grid(w.N, w.lo, w.hi, w.periodic_mask)
+    Rh = make_reward(w)
+    R = torch.from_numpy(Rh).to(dev)
+    V = torch.empty(w.N, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as tdist
+            tdist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch.distributed as tdist
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        capi.vi_solve(g, w.model, w.params, R, V=V, stream=stream)
+    # Table 3's grid shapes (P:468-474): seconds per solve, for context (different, unstated MDP)
+    table3 = {}
+    for name in ("v0", "v1"):
+        wt = VI_CONFIGS[name]
+        gt = capi.Grid(wt.N, wt.lo, wt.hi, wt.periodic_mask)
+        Rt = torch.from_numpy(make_reward(wt)).to(dev)
+        capi.vi_solve(gt, wt.model, wt.params, Rt, stream=stream)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        _, ti = capi.vi_solve(gt, wt.model, wt.params, Rt, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        table3["x".join(map(str, wt.N))] = {"seconds": a.elapsed_time(b) / 1e3, "iterations": ti["iters"]}
+        gt.close()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters, launches = 0, 0
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            _, info = capi.vi_solve(g, w.model, w.params, R, V=V, stream=stream)
+            iters += info["iters"]
+            launches += g.launch_count()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        _, tinfo = capi.vi_solve(g, w.model, w.params, R, V=V, stream=stream, use_graph=False)
+    clocks = clk.summary()
+    total_ms = max_over_ranks(e0.elapsed_time(e1))
+    value = w.points * iters * world / (total_ms / 1e3)
+    Vp = torch.empty(w.N, dtype=torch.float32).pin_memory()
+    Rp = torch.from_numpy(Rh).pin_memory()
+    capi.vi_solve_host(g, w.model, w.params, Rp.numpy(), V=Vp.numpy())
+    barrier()
+    t0 = time.perf_counter()
+    e2e_it = 0
+    for _ in range(max(1, min(args.steps, 3))):
+        _, hi = capi.vi_solve_host(g, w.model, w.params, Rp.numpy(), V=Vp.numpy())
+        e2e_it += hi["iters"]
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    peak, peak_kind = measured_peaks()
+    it_ms = tinfo["iter_ms"] / tinfo["iters"]
+    achieved = VI_BYTES * w.points / (it_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(f"{w.name}:vi")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": VI_METRIC, "value": value, "unit": VI_UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": w.name, "grid": list(w.N), "points": w.points, "model": w.model,
+                   "params": list(w.params), "threshold": 1e-6, "iterations_per_step": iters / args.steps,
+                   "order": "Jacobi (reading A38)",
+                   "l2": ("inputs larger than L2: R + 2 iterates = %.0f MB per iteration vs 126 MB L2" %
+                          (w.points * 12 / 1e6)) if w.points * 12 > 126e6 else "fits L2",
+                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                   "table3_shapes": table3},
+        "roofline": {"bound": "hbm", "kernel": "k_vi_march (Alg. 1 l.4-8, one Bellman iteration)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_kind": peak_kind, "bytes_per_point": VI_BYTES, "avg_launch_ms": it_ms},
+        "clocks": clocks,
+        "e2e": {"value": w.points * e2e_it * world / e2e_s, "unit": VI_UNIT, "h2d_bytes_per_step": w.points * 4,
+                "d2h_bytes_per_step": w.points * 4},
+        "gpu_launches": launches,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, sample, cores, el, work = vi_oracle_sample(w, target_s=args.ref_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": VI_UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    g.close()
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
+def run_vi_reference(args):
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+        if rank != 0:
+            dist.barrier()
+            return
+    from inputs import VI_CONFIGS
+    w = VI_CONFIGS[args.config]
+    times, work = [], []
+    for i in range(args.warmup + args.steps):
+        rate, sample, cores, el, wk = vi_oracle_sample(w, target_s=args.ref_seconds)
+        if i >= args.warmup:
+            times.append(el)
+            work.append(wk)
+    value = sum(work) / sum(times)
+    line = {"impl": "reference", "metric": VI_METRIC, "value": value, "unit": VI_UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "grid": list(w.N)},
+            "cpu_baseline": {"value": value, "unit": VI_UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": VI_UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
 def run_reference(args):
     rank, world, local = dist_env()
     if world > 1:
@@ -507,9 +686,11 @@ def main():
                     help="also time the single-pass variant (SURVEY.md §8(f1)) and report it beside the headline")
     ap.add_argument("--ref-seconds", type=float, default=15.0)
     args = ap.parse_args()
-    from inputs import TTR_CONFIGS
+    from inputs import TTR_CONFIGS, VI_CONFIGS
     if args.config in TTR_CONFIGS:
         (run_ttr_reference if args.impl == "reference" else run_ttr)(args)
+    elif args.config in VI_CONFIGS:
+        (run_vi_reference if args.impl == "reference" else run_vi)(args)
     elif args.impl == "reference":
         run_reference(args)
     else:
