@@ -277,6 +277,158 @@ __global__ void __launch_bounds__(256) k_ttr_march(GridDev g, FParams fp, const 
     if (last_launch) ttr_last_cta_control(st, par);
 }
 
+// l.5-12 for NDIM >= 3 with an in-plane tile in shared memory: CTA = TY x TX nodes of the plane
+// (axes n-2, n-1) for fixed middle-axis indices, marching axis 0 over a segment.  Each step stages
+// the (TY+2) x (TX+2) tile of the next plane (halo wrapped on periodic axes), so the in-plane
+// neighbours are LDS with constant offsets; axis-0 neighbours stay in registers (vm, vc) and the
+// next plane's centre (vn) comes from the staged tile; middle axes (NDIM >= 4) through L1/L2.
+constexpr int TTR_TX = 32, TTR_TY = 8;
+
+template <class F, int NDIM>
+__global__ void __launch_bounds__(TTR_TX * TTR_TY) k_ttr_tile(GridDev g, FParams fp, const float *__restrict__ src,
+                                                              float *__restrict__ dst, TtrState *st, int par,
+                                                              int last_launch, int seg_len, int ntx, int nty) {
+    if (st->done) return;
+    constexpr int A = NDIM - 2, B = NDIM - 1;            // tile axes (rows, columns)
+    constexpr int SW = TTR_TX + 2, SH = TTR_TY + 2;
+    __shared__ float tile[3][SH * SW];
+    F f;
+    {
+        float mn[MAXD], mx[MAXD];
+#pragma unroll
+        for (int d = 0; d < MAXD; ++d) { mn[d] = -1.f; mx[d] = 1.f; }        // A33: costate box [-1, 1]^n
+        f.init(fp, mn, mx);
+    }
+    const int NA = g.N[A], NB = g.N[B];
+    const int N0 = g.N[0];
+    // block -> (tile column, tile row, middle-axis combination); blockIdx.y = axis-0 segment
+    int bx = blockIdx.x;
+    const int tcx = bx % ntx; bx /= ntx;
+    const int tcy = bx % nty; bx /= nty;
+    int idx[NDIM];
+    long long mid = 0;                                   // offset of the middle-axis indices
+#pragma unroll
+    for (int d = A - 1; d >= 1; --d) {
+        idx[d] = bx % g.N[d];
+        bx /= g.N[d];
+        mid += (long long)idx[d] * g.stride[d];
+    }
+    const int tx = threadIdx.x % TTR_TX, ty = threadIdx.x / TTR_TX;
+    const int jb = tcx * TTR_TX + tx, ja = tcy * TTR_TY + ty;    // this thread's node in the plane
+    idx[A] = ja; idx[B] = jb;
+    const bool inside = ja < NA && jb < NB;
+    bool face = !inside;
+    if (inside) {
+#pragma unroll
+        for (int d = 1; d < NDIM; ++d) face |= !g.per[d] && (idx[d] == 0 || idx[d] == g.N[d] - 1);
+    }
+    const long long s0 = g.stride[0];
+    const int sA = (int)g.stride[A];
+    const int a0 = blockIdx.y * seg_len, a1 = min(N0, a0 + seg_len);
+    const bool per0 = g.per[0] != 0;
+    // tile loader: this thread's (at most 2) tile elements, in-plane offsets fixed per CTA (halo
+    // wrapped on periodic axes, clamped on the others: those values are only read by face nodes,
+    // which are not updated here); cp.async into a 3-stage ring, one commit group per plane
+    constexpr int NT = TTR_TX * TTR_TY, NE = (SH * SW + NT - 1) / NT;
+    int eoff[NE];
+    bool eok[NE];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        const int e = threadIdx.x + k * NT;
+        eok[k] = e < SH * SW;
+        const int r = e / SW, cc = e - r * SW;
+        int ga = tcy * TTR_TY + r - 1, gb = tcx * TTR_TX + cc - 1;
+        if (g.per[A]) ga = ga < 0 ? ga + NA : (ga >= NA ? ga - NA : ga); else ga = max(0, min(NA - 1, ga));
+        if (g.per[B]) gb = gb < 0 ? gb + NB : (gb >= NB ? gb - NB : gb); else gb = max(0, min(NB - 1, gb));
+        eoff[k] = ga * sA + gb;
+    }
+    auto at0 = [&](int i0) -> int {                      // wrapped / clamped plane index
+        if (per0) return i0 < 0 ? i0 + N0 : (i0 >= N0 ? i0 - N0 : i0);
+        return max(0, min(N0 - 1, i0));
+    };
+    const uint32_t tb0 = (uint32_t)__cvta_generic_to_shared(&tile[0][0]);
+    constexpr uint32_t TB = 4u * SH * SW;                // bytes per stage
+    auto issue = [&](uint32_t sb, const float *pl) {
+#pragma unroll
+        for (int k = 0; k < NE; ++k)
+            if (eok[k])
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sb + 4u * (uint32_t)(threadIdx.x + k * NT)),
+                             "l"(pl + eoff[k]) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto plane = [&](int i0) -> const float * { return src + (long long)at0(i0) * s0 + mid; };
+    Pt q;
+    if (inside) {
+#pragma unroll
+        for (int d = 1; d < NDIM; ++d) load_axis<F>(g, q, d, idx[d]);
+    }
+    const uint32_t ctr4 = 4u * (uint32_t)((ty + 1) * SW + tx + 1);
+    const long long me = mid + (long long)ja * sA + jb;  // in-plane element of this thread's node
+    float cmax = 0.f;
+    float vm = 0.f, vc = 0.f;
+    if (inside) vm = fabsf(src[(long long)at0(a0 - 1) * s0 + me]);
+    uint32_t sc = tb0, sn = tb0 + TB, sf = tb0 + 2 * TB;   // stages: plane i0, i0 + 1, i0 + 2
+    issue(sc, plane(a0));
+    issue(sn, plane(a0 + 1));
+    const float *pf = plane(a0 + 2);                     // next plane to fetch (interior: +s0 per step)
+    float *dp = dst + (long long)a0 * s0 + me;
+    auto ld = [](uint32_t addr) -> float {
+        float v;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+        return v;
+    };
+    for (int i0 = a0; i0 < a1; ++i0, dp += s0) {
+        issue(sf, pf);                                   // (a group is committed even past the segment)
+        pf = (i0 + 3 < N0) ? pf + s0 : plane(i0 + 3);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");   // planes i0 and i0 + 1 have landed
+        __syncthreads();
+        if (inside) {
+            if (i0 == a0) vc = ld(sc + ctr4);
+            const float vn = ld(sn + ctr4);
+            const float old = vc;
+            float v = old;
+            if (!face && !is_target(old) && (per0 || (i0 != 0 && i0 != N0 - 1))) {
+                load_axis<F>(g, q, 0, i0);
+                float p[NDIM];
+                float num = 0.f, den = 0.f;
+#pragma unroll
+                for (int d = 0; d < NDIM; ++d) {
+                    float vp, vmd;
+                    if (d == 0) { vp = fabsf(vn); vmd = vm; }
+                    else if (d == A) { vp = fabsf(ld(sc + ctr4 + 4u * SW)); vmd = fabsf(ld(sc + ctr4 - 4u * SW)); }
+                    else if (d == B) { vp = fabsf(ld(sc + ctr4 + 4u)); vmd = fabsf(ld(sc + ctr4 - 4u)); }
+                    else {
+                        const long long sd = g.stride[d];
+                        long long op = sd, om = -sd;
+                        if (g.per[d]) {
+                            if (idx[d] == g.N[d] - 1) op = -(long long)(g.N[d] - 1) * sd;
+                            if (idx[d] == 0) om = (long long)(g.N[d] - 1) * sd;
+                        }
+                        const float *pc = src + (dp - dst);
+                        vp = fabsf(pc[op]); vmd = fabsf(pc[om]);
+                    }
+                    p[d] = (vp - vmd) * g.hih[d];        // central difference (A32)
+                    const float a = f.alpha(d, q);
+                    num = fmaf(a * g.hih[d], vp + vmd, num);
+                    den = fmaf(a, g.inv_dx[d], den);
+                }
+                const float H = -f.ham(q, p) - 1.f;      // A32: H_TTR = -H_reach(goal -1) - 1
+                const float nv = den > 0.f ? (num - H) / den : old;   // l.10-11 (A33)
+                v = fminf(nv, old) + 0.f;                // l.12
+                cmax = fmaxf(cmax, fabsf(v - old));
+            }
+            *dp = v;                                     // (A34: target / faces keep their value)
+            vm = fabsf(vc);
+            vc = vn;
+        }
+        __syncthreads();                                 // stage sc is refilled by the next issue
+        const uint32_t t = sc; sc = sn; sn = sf; sf = t;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    ttr_reduce_change(cmax, st, par);
+    if (last_launch) ttr_last_cta_control(st, par);
+}
+
 // l.14-15 along axis d on its two faces, in place in dst (which holds the interior update and the
 // rules of axes < d; face nodes were copied from src by k_ttr_rows).  The rule reads the nodes 1 and
 // 2 cells inside, never on an axis-d face (N >= 4), so no value this launch writes is read.  Nodes
@@ -325,10 +477,12 @@ typedef void (*ttr_rows_fn)(GridDev, FParams, const float *, float *, TtrState *
 typedef void (*ttr_face_fn)(GridDev, int, int, const float *, float *, TtrState *, int);
 
 typedef void (*ttr_march_fn)(GridDev, FParams, const float *, float *, TtrState *, int, int, int);
+typedef void (*ttr_tile_fn)(GridDev, FParams, const float *, float *, TtrState *, int, int, int, int, int);
 
 struct TtrFns {
     ttr_rows_fn rows = nullptr;       // NDIM == 1
     ttr_march_fn march = nullptr;     // NDIM >= 2
+    ttr_tile_fn tile = nullptr;       // NDIM >= 3
     ttr_face_fn face = nullptr;
 };
 
@@ -337,6 +491,7 @@ static TtrFns ttr_fns() {
     TtrFns t;
     if constexpr (NDIM == 1) t.rows = k_ttr_rows<F, NDIM>;
     else t.march = k_ttr_march<F, NDIM>;
+    if constexpr (NDIM >= 3) t.tile = k_ttr_tile<F, NDIM>;
     t.face = k_ttr_face<NDIM>;
     return t;
 }

@@ -1248,6 +1248,20 @@ static odp_status ttr_device(odp_grid *g, int dyn, const double *params, int npa
     const int seg_len = (int)((g->n0 + nseg - 1) / nseg);
     nseg = (int)((g->n0 + seg_len - 1) / seg_len);
     const dim3 grid_march(col_blocks, nseg);
+    // tile kernel (NDIM >= 3): TY x TX in-plane tiles x middle-axis combinations x axis-0 segments
+    const bool use_tile = fn.tile != nullptr && !(getenv("ODP_TTR_TILE") && atoi(getenv("ODP_TTR_TILE")) == 0);
+    int ntx = 1, nty = 1, tile_seg = 1;
+    dim3 grid_tile(1, 1);
+    if (use_tile) {
+        ntx = (int)((g->N[n - 1] + TTR_TX - 1) / TTR_TX);
+        nty = (int)((g->N[n - 2] + TTR_TY - 1) / TTR_TY);
+        long long nb = (long long)ntx * nty;
+        for (int d = 1; d < n - 2; ++d) nb *= g->N[d];
+        int ns = (int)std::max<long long>(1, std::min<long long>(g->n0, ((long long)nsm * 6 + nb - 1) / nb));
+        tile_seg = (int)((g->n0 + ns - 1) / ns);
+        ns = (int)((g->n0 + tile_seg - 1) / tile_seg);
+        grid_tile = dim3((unsigned)nb, (unsigned)ns);
+    }
     int grid_face[MAXD] = {0}, last_axis = -1;
     for (int d = 0; d < n; ++d) {
         grid_face[d] = (int)std::min<long long>((2 * (P / g->N[d]) + block - 1) / block, (long long)nsm * 8);
@@ -1268,7 +1282,9 @@ static odp_status ttr_device(odp_grid *g, int dyn, const double *params, int npa
         const float *src = buf[k & 1];
         float *dst = buf[par];
         if (ev) cudaEventRecord(ev[0], s);
-        if (fn.march) fn.march<<<grid_march, block, 0, s>>>(gd, fp, src, dst, g->d_ttr, par, last_axis < 0 ? 1 : 0, seg_len);
+        if (use_tile) fn.tile<<<grid_tile, TTR_TX * TTR_TY, 0, s>>>(gd, fp, src, dst, g->d_ttr, par, last_axis < 0 ? 1 : 0,
+                                                                  tile_seg, ntx, nty);
+        else if (fn.march) fn.march<<<grid_march, block, 0, s>>>(gd, fp, src, dst, g->d_ttr, par, last_axis < 0 ? 1 : 0, seg_len);
         else fn.rows<<<grid_rows, block, 0, s>>>(gd, fp, src, dst, g->d_ttr, par, last_axis < 0 ? 1 : 0);
         if (ev) cudaEventRecord(ev[1], s);
         for (int d = 0; d < n; ++d)
