@@ -57,7 +57,9 @@ if os.path.exists(rep):
         traffic[f"c4:{kind}"] = rd_b + wr_b
         traffic[f"c4:{kind}:kernel"] = re.sub(r"\(.*", "", d["Kernel Name"])
     traffic["_source"] = f"profiles/{tag}_ncu_full_summary.txt (dram__bytes_read.sum + dram__bytes_write.sum, one launch each)"
-    json.dump(traffic, open("profiles/ncu_traffic.json", "w"), indent=1)
+    old = json.load(open("profiles/ncu_traffic.json")) if os.path.exists("profiles/ncu_traffic.json") else {}
+    old.update(traffic)                     # keep the other workloads' entries (t1, v2)
+    json.dump(old, open("profiles/ncu_traffic.json", "w"), indent=1)
 if os.path.exists(os.path.join(src, "bench.json")):
     shutil.copy(os.path.join(src, "bench.json"), f"profiles/{tag}_bench.json")
 print(open(f"profiles/{tag}_launch_shares.txt").read())
