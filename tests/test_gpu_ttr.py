@@ -176,3 +176,19 @@ def test_ttr_t1_full_size_fixed_point():
                        indexing="ij")
     dist = np.maximum(np.sqrt(X ** 2 + Y ** 2) - 1.0, 0.0)[:, :, None]
     assert np.all(out[1:-1, 1:-1] >= dist[1:-1, 1:-1] - 0.1)
+
+
+@pytest.mark.parametrize("N", [(24, 20), (12, 10, 14)])
+def test_ttr_all_periodic_axes(N):
+    # no faces at all: the interior launch is the iteration's last launch and runs the stop test
+    n = len(N)
+    per = (1,) * n
+    lo, hi = (-2.0,) * n, (2.0,) * n
+    axes = [axis_nodes(N[d], lo[d], hi[d], True) for d in range(n)]
+    X = np.meshgrid(*axes, indexing="ij")
+    V0 = (np.sqrt(sum(x ** 2 for x in X)) - 0.6).astype(np.float32)
+    ref, _, _ = oracle.ttr_solve(N, lo, hi, (1 << n) - 1, "HOLONOMIC_BALL", (1.0, -1.0), V0, eps=1e-12,
+                                 max_sweeps=20000)
+    out, info = _gpu(N, lo, hi, per, "HOLONOMIC_BALL", (1.0, -1.0), V0, eps=1e-7)
+    np.testing.assert_allclose(out, ref, atol=_tol(ref), rtol=0)
+    assert info["last_change"] <= 1e-7
