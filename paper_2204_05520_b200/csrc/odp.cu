@@ -489,6 +489,8 @@ struct odp_grid {
     cudaStream_t own_stream = nullptr;
     std::vector<cudaEvent_t> events;
     long long launches = 0;
+    float *d_stage = nullptr;     // staging buffers of the *_host entry points (grown on demand)
+    size_t stage_elems = 0;
     TtrState *d_ttr = nullptr;    // time-to-reach iteration state (odp_ttr_solve)
     TtrState *h_ttr = nullptr;    // pinned
 };
@@ -506,6 +508,8 @@ static void free_device(odp_grid *g) {
     if (g->h_state) cudaFreeHost(g->h_state);
     cudaFree(g->d_ttr);
     if (g->h_ttr) cudaFreeHost(g->h_ttr);
+    cudaFree(g->d_stage);
+    g->d_stage = nullptr; g->stage_elems = 0;
     g->d_ttr = nullptr; g->h_ttr = nullptr;
     if (g->own_stream) cudaStreamDestroy(g->own_stream);
     for (auto e : g->events) cudaEventDestroy(e);
@@ -670,6 +674,20 @@ static odp_status ensure_device(odp_grid *g, int nparts_needed) {
     }
     if (!g->d_range) CUDA_TRY(cudaMalloc(&g->d_range, (2 * MAXD + 2) * sizeof(float)));
     if (!g->d_amax) CUDA_TRY(cudaMalloc(&g->d_amax, 1024 * MAXD * sizeof(float)));
+    return ODP_OK;
+}
+
+// Device staging area of the *_host entry points: kept in the handle so that repeated end-to-end
+// calls do not pay a multi-GB allocation each time.
+static odp_status stage_buffer(odp_grid *g, size_t elems, float **out) {
+    if (g->stage_elems < elems) {
+        cudaFree(g->d_stage);
+        g->d_stage = nullptr;
+        g->stage_elems = 0;
+        CUDA_TRY(cudaMalloc(&g->d_stage, elems * sizeof(float)));
+        g->stage_elems = elems;
+    }
+    *out = g->d_stage;
     return ODP_OK;
 }
 
@@ -1079,17 +1097,17 @@ extern "C" odp_status odp_hj_solve_host(odp_grid *g, int dynamics_id, const doub
     if (!V0 || !out) return fail(ODP_EINVAL, "NULL V0/out");
     if ((st = ensure_device(g, 1))) return st;
     const int nout = (opts && opts->write_initial) ? ntau : ntau - 1;
-    const size_t bytes = (size_t)local_points(g) * sizeof(float);
+    const size_t P = (size_t)local_points(g), bytes = P * sizeof(float);
     cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
-    float *dV0 = nullptr, *dout = nullptr, *dT = nullptr;
-    CUDA_TRY(cudaMallocAsync(&dV0, bytes, s));
-    CUDA_TRY(cudaMallocAsync(&dout, bytes * nout, s));
+    const bool has_t = opts && opts->target;
+    float *base = nullptr;
+    if ((st = stage_buffer(g, P * (size_t)(1 + nout + (has_t ? 1 : 0)), &base))) return st;
+    float *dV0 = base, *dout = base + P, *dT = has_t ? base + P * (size_t)(1 + nout) : nullptr;
     odp_solve_opts o;
     memset(&o, 0, sizeof o);
     if (opts) o = *opts;
     o.stream = s;
-    if (opts && opts->target) {
-        CUDA_TRY(cudaMallocAsync(&dT, bytes, s));
+    if (has_t) {
         CUDA_TRY(cudaMemcpyAsync(dT, opts->target, bytes, cudaMemcpyHostToDevice, s));
         o.target = dT;
     }
@@ -1100,9 +1118,6 @@ extern "C" odp_status odp_hj_solve_host(odp_grid *g, int dynamics_id, const doub
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess && st == ODP_OK) st = fail(ODP_ECUDA, "copy out: %s", cudaGetErrorString(e));
     }
-    cudaFreeAsync(dV0, s);
-    cudaFreeAsync(dout, s);
-    if (dT) cudaFreeAsync(dT, s);
     cudaStreamSynchronize(s);
     return st;
 }
@@ -1324,8 +1339,8 @@ extern "C" odp_status odp_ttr_solve_host(odp_grid *g, int dynamics_id, const dou
     const size_t bytes = (size_t)local_points(g) * sizeof(float);
     cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
     float *dV0 = nullptr, *dphi = nullptr;
-    CUDA_TRY(cudaMallocAsync(&dV0, bytes, s));
-    CUDA_TRY(cudaMallocAsync(&dphi, bytes, s));
+    if ((st = stage_buffer(g, 2 * (size_t)local_points(g), &dV0))) return st;
+    dphi = dV0 + local_points(g);
     odp_ttr_opts o;
     memset(&o, 0, sizeof o);
     if (opts) o = *opts; else o.use_graph = 1;
@@ -1337,8 +1352,6 @@ extern "C" odp_status odp_ttr_solve_host(odp_grid *g, int dynamics_id, const dou
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) st = fail(ODP_ECUDA, "copy out: %s", cudaGetErrorString(e));
     }
-    cudaFreeAsync(dV0, s);
-    cudaFreeAsync(dphi, s);
     cudaStreamSynchronize(s);
     return st;
 }
@@ -1440,8 +1453,8 @@ extern "C" odp_status odp_vi_solve_host(odp_grid *g, int model_id, const double 
     const size_t bytes = (size_t)local_points(g) * sizeof(float);
     cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
     float *dR = nullptr, *dV = nullptr;
-    CUDA_TRY(cudaMallocAsync(&dR, bytes, s));
-    CUDA_TRY(cudaMallocAsync(&dV, bytes, s));
+    if ((st = stage_buffer(g, 2 * (size_t)local_points(g), &dR))) return st;
+    dV = dR + local_points(g);
     odp_vi_opts o;
     memset(&o, 0, sizeof o);
     if (opts) o = *opts; else o.use_graph = 1;
@@ -1453,8 +1466,6 @@ extern "C" odp_status odp_vi_solve_host(odp_grid *g, int model_id, const double 
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) st = fail(ODP_ECUDA, "copy out: %s", cudaGetErrorString(e));
     }
-    cudaFreeAsync(dR, s);
-    cudaFreeAsync(dV, s);
     cudaStreamSynchronize(s);
     return st;
 }
