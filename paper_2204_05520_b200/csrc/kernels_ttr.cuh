@@ -442,32 +442,41 @@ __global__ void __launch_bounds__(256) k_ttr_face(GridDev g, int d, int last_lau
     const long long outer = g.P / (inner * Nd);
     const long long per_side = outer * inner;
     float cmax = 0.f;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * per_side; t += stride) {
-        const int side = t >= per_side;
-        const long long r = side ? t - per_side : t;
-        const long long o = r / inner, in = r - o * inner;
-        const long long i = o * (inner * Nd) + (side ? (long long)(Nd - 1) * inner : 0) + in;
+    // index arithmetic in 32 bits when the face set and the element offsets fit (the usual case)
+    auto body = [&](auto t, auto per_side_, auto inner_) {
+        using I = decltype(t);
+        const int side = t >= per_side_;
+        const I r = side ? t - per_side_ : t;
+        const I o = r / inner_, in = r - o * inner_;
+        const long long i = (long long)o * ((long long)inner_ * Nd) + (side ? (long long)(Nd - 1) * inner_ : 0) + in;
         const float cur = dst[i];
         float v = cur;
         if (!is_target(cur)) {                           // A34: target nodes keep 0
-            const long long sa = side ? -inner : inner;
+            const long long sa = side ? -(long long)inner_ : (long long)inner_;
             const float a = fabsf(dst[i + sa]), b = fabsf(dst[i + 2 * sa]);
             v = fminf(fmaxf(2.f * a - b, b), cur) + 0.f;
             dst[i] = v;
         }
         // highest face axis of this node: the axes e > d are decoded from `in`
         bool last = true;
-        long long rem = in;
+        I rem = in;
 #pragma unroll
         for (int e = NDIM - 1; e > 0; --e) {
             if (e <= d) break;
-            const long long q = rem / g.N[e];
-            const int ie = (int)(rem - q * g.N[e]);
+            const I q = rem / (I)g.N[e];
+            const int ie = (int)(rem - q * (I)g.N[e]);
             rem = q;
             if (!g.per[e] && (ie == 0 || ie == g.N[e] - 1)) last = false;
         }
         if (last) cmax = fmaxf(cmax, fabsf(v - src[i]));
+    };
+    if (2 * per_side < (1LL << 31)) {
+        const unsigned ps = (unsigned)per_side, inn = (unsigned)inner, tot = 2u * ps;
+        for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) body(t, ps, inn);
+    } else {
+        const long long stride = (long long)gridDim.x * blockDim.x;
+        for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * per_side; t += stride)
+            body(t, per_side, inner);
     }
     ttr_reduce_change(cmax, st, par);
     if (last_launch) ttr_last_cta_control(st, par);
