@@ -39,6 +39,26 @@ PASS2_BYTES = {("low", "brt"): 12, ("low", "brs"): 8,          # Euler: R W, (R 
 STAGE_BYTES = {("low", "brt"): 16, ("low", "brs"): 12, ("medium", "brt"): 16, ("medium", "brs"): 14}
 
 
+# The march kernels read every W tile through L2 several times: per node and pass,
+# 2R+1 ... tiles of the side axes.  L2-to-SM bytes per point: pass 1 = (1 centre + (2R-1 interior
+# edge-assigned side tiles) x side axes) x 4 B; pass 2 = (1 + 2R x side axes) x 4 B of W plus the
+# Vn / target / output streams (mean of the RK stages).  Cap: the LTS throughput of
+# /opt/skills/guides/B300_MICROARCH.md (~6300 B/cycle full chip) at the measured SM clock.
+def l2_path(w, pass1_ms, pass2_ms, Pl, sm_mhz=1900.0):
+    n = len(w.N)
+    R = 1 if w.accuracy == "low" else 2
+    side = max(0, n - 3)
+    p1 = (1 + (2 * R - (1 if R == 2 else 0)) * side) * 4
+    extra = {("low", "brt"): 8, ("low", "brs"): 4, ("medium", "brt"): 10, ("medium", "brs"): 8}[(w.accuracy, w.mode)]
+    p2 = (1 + 2 * R * side) * 4 + extra
+    cap = 6300.0 * sm_mhz * 1e6 / 1e12
+    a1 = p1 * Pl / (pass1_ms / 1e3) / 1e12
+    a2 = p2 * Pl / (pass2_ms / 1e3) / 1e12
+    return {"unit": "TB/s", "cap": cap, "pass1_bytes_per_point": p1, "pass1_achieved": a1, "pass1_frac": a1 / cap,
+            "pass2_bytes_per_point": p2, "pass2_achieved": a2, "pass2_frac": a2 / cap,
+            "note": "L2-to-SM tile traffic of the march kernels vs the LTS throughput cap (context for the HBM frac)"}
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -634,7 +654,8 @@ def run_ours(args):
                      "traffic": traffic, "peak_kind": peak_kind,
                      "bytes_per_point": PASS2_BYTES[key], "avg_launch_ms": pass2_ms,
                      "stage": {"bytes_per_point": STAGE_BYTES[key], "achieved": stage_gbs,
-                               "frac": stage_gbs / peak, "pass1_ms": pass1_ms}},
+                               "frac": stage_gbs / peak, "pass1_ms": pass1_ms},
+                     "l2_path": l2_path(w, pass1_ms, pass2_ms, Pl, clocks.get("sm_mhz") or 1900.0)},
         "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": Pl * 4 * world,
                 "d2h_bytes_per_step": Pl * 4 * nout * world},
