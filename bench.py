@@ -285,7 +285,7 @@ def run_ttr(args):
                    "l2": ("inputs larger than L2: 2 x %.0f MB iterates (%.0f MB) per iteration vs 126 MB L2" %
                           (w.points * 4 / 1e6, w.points * 8 / 1e6)) if w.points * 8 > 126e6 else "iterates fit L2",
                    "parallelism": "single GPU" if world == 1 else f"{world} independent replicas"},
-        "roofline": {"bound": "hbm", "kernel": "k_ttr_march (Alg. 3 l.5-12, interior update)",
+        "roofline": {"bound": "hbm", "kernel": ("k_ttr_tile" if len(w.N) >= 3 else "k_ttr_march") + " (Alg. 3 l.5-12, interior update)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_kind": peak_kind, "bytes_per_point": TTR_BYTES,
                      "avg_launch_ms": interior_ms, "faces_ms_per_iteration": faces_ms},
