@@ -286,6 +286,10 @@ struct MarchArgs {
     int ncols;            // columns (product of the side extents)
     int dbg;              // experiments only (ODP_MARCH_DBG): 2 = skip the arithmetic, 4 = skip the copies
     int K, nseg, units;   // marching segment length, segments per column, work units
+    // axis-0 subset of the columns (multi-GPU overlap): 0 all, 1 interior planes
+    // [i0r, N0 - i0r), 2 boundary planes [0, i0r) and [N0 - i0r, N0); s0n = planes in the subset
+    int i0map, i0r, s0n;
+    int wslot;            // dynamic work counter of this launch (st->work[wslot])
 };
 constexpr int MARCH_SMARG = 4;   // leading margin of a side slot (floats)
 
@@ -321,16 +325,22 @@ struct MarchUnit {
 // axis 2 inside blocks of b1 consecutive axis-1 indices, so the +-2 neighbourhood of a wave stays
 // resident in the 126 MB L2 instead of being re-read from HBM (ncu: 5.2x algorithmic DRAM bytes
 // with the memory order).  Returns the memory-order column index.
+__device__ __forceinline__ int march_i0(const MarchArgs &a, int i) {   // subset index -> axis-0 plane
+    if (a.i0map == 1) return i + a.i0r;
+    if (a.i0map == 2) return i < a.i0r ? i : a.sn[0] - 2 * a.i0r + i;
+    return i;
+}
+
 template <int MA>
 __device__ __forceinline__ int march_col(const MarchArgs &a, int c) {
     if constexpr (MA <= 1) {
-        return c;
+        return march_i0(a, c);
     } else if constexpr (MA == 2) {
-        const int i0 = c % a.sn[0], i1 = c / a.sn[0];
+        const int i0 = march_i0(a, c % a.s0n), i1 = c / a.s0n;
         return i0 * a.sn[1] + i1;
     } else {
-        const int i0 = c % a.sn[0];
-        int r = c / a.sn[0];
+        const int i0 = march_i0(a, c % a.s0n);
+        int r = c / a.s0n;
         const int i1l = r % a.b1;
         r /= a.b1;
         const int i2 = r % a.sn[2];
@@ -386,8 +396,10 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     static_assert(NP == 1, "the march family computes node pairs (VEC = 2)");
     // dynamic work distribution: pass 1 takes units from work[0], pass 2 from work[1]; each pass
     // resets the other pass's counter (that launch has completed: same stream)
-    unsigned int *wctr = const_cast<unsigned int *>(&st->work[PASS2 ? 1 : 0]);
-    if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<DevState *>(st)->work[PASS2 ? 0 : 1] = 0u;
+    unsigned int *wctr = const_cast<unsigned int *>(&st->work[a.wslot]);
+    if (blockIdx.x == 0 && threadIdx.x == 0)          // the other launches' counters (stream order: not running)
+        for (int k = 0; k < 3; ++k)
+            if (k != a.wslot) const_cast<DevState *>(st)->work[k] = 0u;
     if (!st->active) return;
     constexpr int VEC = 2;
     constexpr int NO = NDIM - 2;     // outer axes
@@ -1039,6 +1051,8 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     a.units = (int)(cols_rb * a.nseg);
     a.dbg = 0;
     if (const char *env = getenv("ODP_MARCH_DBG")) a.dbg = atoi(env);
+    a.i0map = 0; a.i0r = 0; a.s0n = a.sn[0];
+    a.wslot = 0;                                    // pass 2 launches use slot 1 (march_pass2)
     p->block = ((a.nthr + 31) / 32) * 32 + 32;      // compute warps + the producer warp
     p->smem = (size_t)geo_smem_bytes(R, N1, best, NSS, nst);
     p->grid = 0;
@@ -1068,7 +1082,31 @@ inline void march_pass1(const MarchFns &t, const MarchPlan &p, const GridDev &g,
 inline void march_pass2(const MarchFns &t, const MarchPlan &p, const GridDev &g, const float *W, const float *Vn,
                         const float *T, float *out, const DevState *st, const FParams &fp, int kind, int brt,
                         cudaStream_t s, float *guard_partials = nullptr) {
-    t.pass2<<<p.grid, p.block, p.smem, s>>>(p.a, g, W, Vn, T, out, guard_partials, st, fp, kind, brt);
+    MarchArgs a = p.a;
+    a.wslot = 1;
+    t.pass2<<<p.grid, p.block, p.smem, s>>>(a, g, W, Vn, T, out, guard_partials, st, fp, kind, brt);
+}
+
+// Pass 1 split by axis-0 planes (multi-GPU overlap): the interior planes [R, N0 - R)
+// need no halo, the boundary planes [0, R) and [N0 - R, N0) do.  Both launches use the full grid so
+// the partials are 2 x grid records (interior first).  map: 1 interior, 2 boundary.
+inline MarchArgs march_subset(const MarchArgs &a0, int map, int R) {
+    MarchArgs a = a0;
+    a.i0map = map;
+    a.i0r = R;
+    a.s0n = map == 1 ? a0.sn[0] - 2 * R : 2 * R;
+    const long long per_plane = a0.ncols / a0.sn[0];
+    a.ncols = (int)(per_plane * a.s0n);
+    a.units = a.ncols * a.nrb * a.nseg;
+    a.wslot = map == 1 ? 0 : 2;
+    return a;
+}
+
+inline void march_pass1_split(const MarchFns &t, const MarchPlan &p, const MarchArgs &a, const GridDev &g,
+                              const float *W, float *partials, const DevState *st, cudaStream_t s) {
+    FParams fp;
+    memset(&fp, 0, sizeof fp);
+    t.pass1<<<p.grid, p.block, p.smem, s>>>(a, g, W, nullptr, nullptr, nullptr, partials, st, fp, 0, 0);
 }
 
 }  // namespace odp

@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(256) k_finalize(const float *__restrict__ part
 __global__ void k_init_state(DevState *st, double cfl, double eps) {
     st->tau = 0.0; st->tau_target = 0.0; st->eps = eps; st->dt = 0.0; st->cfl = cfl; st->dt_f = 0.f;
     st->maxabs = 0.f; st->nan = 0; st->active = 0; st->status = 0; st->steps = 0; st->stages = 0; st->pending = 0;
-    st->work[0] = st->work[1] = 0u;
+    st->work[0] = st->work[1] = st->work[2] = 0u;
     for (int d = 0; d < MAXD; ++d) { st->minD[d] = 0.f; st->maxD[d] = 0.f; st->amax[d] = 0.f; }
 }
 
@@ -487,6 +487,8 @@ struct odp_grid {
     DevState *d_state = nullptr;
     DevState *h_state = nullptr;  // pinned
     cudaStream_t own_stream = nullptr;
+    cudaStream_t side_stream = nullptr;     // NCCL halo exchange overlapped with interior pass 1
+    cudaEvent_t ev_in = nullptr, ev_halo = nullptr;
     std::vector<cudaEvent_t> events;
     long long launches = 0;
     float *d_stage = nullptr;     // staging buffers of the *_host entry points (grown on demand)
@@ -512,6 +514,10 @@ static void free_device(odp_grid *g) {
     g->d_stage = nullptr; g->stage_elems = 0;
     g->d_ttr = nullptr; g->h_ttr = nullptr;
     if (g->own_stream) cudaStreamDestroy(g->own_stream);
+    if (g->side_stream) cudaStreamDestroy(g->side_stream);
+    if (g->ev_in) cudaEventDestroy(g->ev_in);
+    if (g->ev_halo) cudaEventDestroy(g->ev_halo);
+    g->side_stream = nullptr; g->ev_in = nullptr; g->ev_halo = nullptr;
     for (auto e : g->events) cudaEventDestroy(e);
     g->events.clear();
     g->d_tab = nullptr; g->d_dx = nullptr; g->d_buf[0] = g->d_buf[1] = nullptr; g->d_partials = nullptr;
@@ -831,6 +837,25 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
         if ((st = ensure_device(g, tp.grid))) return st;
     }
     const int nparts = use_march ? mp.grid : use_stream ? sp.grid : (use_tiled ? tp.grid : grid_generic);
+    // multi-GPU overlap: pass 1 on the interior axis-0 planes runs while the NCCL halo
+    // exchange is in flight on a side stream, then pass 1 on the R boundary planes at each slab end.
+    // Needs an axis-0 side axis (march family, dims >= 4) and interior planes; ODP_SPLIT_PASS1=1
+    // forces the split on one rank (tests: bitwise equal to the unsplit solve)
+    const bool force_split = getenv("ODP_SPLIT_PASS1") && atoi(getenv("ODP_SPLIT_PASS1")) == 1;
+    const bool split = use_march && n >= 4 && g->n0 >= 2 * R + 1 && (g->nranks > 1 || force_split) &&
+                       !(getenv("ODP_SPLIT_PASS1") && atoi(getenv("ODP_SPLIT_PASS1")) == 0);
+    MarchArgs ma_int, ma_bnd;
+    if (split) {
+        ma_int = march_subset(mp.a, 1, R);
+        ma_bnd = march_subset(mp.a, 2, R);
+        if ((st = ensure_device(g, 2 * mp.grid))) return st;
+        if (!g->side_stream) {
+            CUDA_TRY(cudaStreamCreateWithFlags(&g->side_stream, cudaStreamNonBlocking));
+            CUDA_TRY(cudaEventCreateWithFlags(&g->ev_in, cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&g->ev_halo, cudaEventDisableTiming));
+        }
+    }
+    const int nparts1 = split ? 2 * mp.grid : nparts;      // pass-1 partial records (launch_fin)
 
     cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
     const double cfl = (opts && opts->cfl > 0.0) ? opts->cfl : (accuracy == ODP_LOW ? 0.8 : 0.5);   // A7
@@ -901,15 +926,15 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
     auto launch_fin = [&](int stage_in_step, int final_check) {
         const float *rng = nullptr;
         if (g->comm) {
-            ks.red<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, g->d_range);
+            ks.red<<<1, 256, 0, s>>>(g->d_partials, nparts1, g->d_state, g->d_range);
             if (cst == ODP_OK) cst = range_allreduce(g, n, s);
             rng = g->d_range;
         }
         if (ks.amax3 && stage_in_step == 0 && !final_check) {
-            ks.srange<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, rng);
+            ks.srange<<<1, 256, 0, s>>>(g->d_partials, nparts1, g->d_state, rng);
             ks.amax3<<<namax, 256, 0, s>>>(gd, fp, g->d_state, g->d_amax);
         }
-        ks.fin<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, gd, fp, g->d_dx, stage_in_step, final_check,
+        ks.fin<<<1, 256, 0, s>>>(g->d_partials, nparts1, g->d_state, gd, fp, g->d_dx, stage_in_step, final_check,
                                  rng, g->d_amax, namax);
     };
 
@@ -929,6 +954,27 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
         if (timed) CUDA_TRY(cudaEventRecord(g->events[ev + 1], s));
         launches.push_back({kind, ev});
         return ODP_OK;
+    };
+
+    // the stage's halo exchange + pass 1: overlapped (split) or in sequence
+    auto split_pass1 = [&](float *Wx) {
+        cudaEventRecord(g->ev_in, s);                    // W complete (previous pass 2)
+        cudaStreamWaitEvent(g->side_stream, g->ev_in, 0);
+        if (g->nranks > 1 && cst == ODP_OK) cst = halo_exchange(g, Wx, R, g->side_stream);
+        cudaEventRecord(g->ev_halo, g->side_stream);
+        march_pass1_split(mfn, mp, ma_int, gd, Wx, g->d_partials, g->d_state, s);
+        cudaStreamWaitEvent(s, g->ev_halo, 0);
+        march_pass1_split(mfn, mp, ma_bnd, gd, Wx, g->d_partials + (size_t)mp.grid * (2 * n + 2), g->d_state, s);
+    };
+    auto exch_pass1 = [&](float *Wx) -> odp_status {
+        odp_status r = ODP_OK;
+        if (split) {
+            r = rec(0, [&] { split_pass1(Wx); });
+            ++g->launches;                                // two pass-1 launches (rec counts one)
+            return r;
+        }
+        if (g->nranks > 1 && (r = rec(2, [&] { exch(Wx); }))) return r;
+        return rec(0, [&] { launch_pass1(Wx); });
     };
 
     int cur = 0;                       // index of the buffer holding the current V
@@ -953,17 +999,14 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
                 if ((r = rec(2, [&] { launch_guard(1); }))) return r;
             }
         } else if (accuracy == ODP_LOW) {
-            if (g->nranks > 1 && (r = rec(2, [&] { exch(buf[a]); }))) return r;
-            if ((r = rec(0, [&] { launch_pass1(buf[a]); }))) return r;
+            if ((r = exch_pass1(buf[a]))) return r;
             if ((r = rec(2, [&] { launch_fin(0, 0); }))) return r;
             if ((r = rec(1, [&] { launch_pass2(buf[a], nullptr, buf[b], STAGE_EULER); }))) return r;
         } else {
-            if (g->nranks > 1 && (r = rec(2, [&] { exch(buf[0]); }))) return r;
-            if ((r = rec(0, [&] { launch_pass1(buf[0]); }))) return r;
+            if ((r = exch_pass1(buf[0]))) return r;
             if ((r = rec(2, [&] { launch_fin(0, 0); }))) return r;
             if ((r = rec(1, [&] { launch_pass2(buf[0], nullptr, buf[1], STAGE_RK1); }))) return r;
-            if (g->nranks > 1 && (r = rec(2, [&] { exch(buf[1]); }))) return r;
-            if ((r = rec(0, [&] { launch_pass1(buf[1]); }))) return r;
+            if ((r = exch_pass1(buf[1]))) return r;
             if ((r = rec(2, [&] { launch_fin(1, 0); }))) return r;
             if ((r = rec(1, [&] { launch_pass2(buf[1], buf[0], buf[0], STAGE_RK2); }))) return r;
         }
@@ -1059,8 +1102,13 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
         // final guard on the last V (reading A19)
         const float *Wf = buf[accuracy == ODP_LOW ? cur : 0];
         k_force_active<<<1, 1, 0, s>>>(g->d_state);
-        exch(const_cast<float *>(Wf));
-        launch_pass1(Wf);
+        if (split) {
+            split_pass1(const_cast<float *>(Wf));
+            ++g->launches;
+        } else {
+            exch(const_cast<float *>(Wf));
+            launch_pass1(Wf);
+        }
         launch_fin(0, 1);
         if (cst) return cst;
         g->launches += 3;

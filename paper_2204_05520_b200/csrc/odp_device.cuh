@@ -49,7 +49,7 @@ struct DevState {
     int active;          // 1 while the current save interval still needs steps
     int status;          // 0 ok, 2 numeric failure (A19)
     int pending;         // single-pass: the last stage's OUTPUT failed the guard; fail at the next stage's start
-    unsigned int work[2];  // dynamic work counters of the march pass-1 / pass-2 launches (each resets the other's)
+    unsigned int work[3];  // dynamic work counters of the march launches: pass 1, pass 2, split pass 1 (boundary)
     long long steps, stages;
 };
 

@@ -64,3 +64,39 @@ def test_single_pass_guard_reports_divergence():
     assert info["single_pass"]
     assert info["steps"] == tinfo["steps"] == ref.steps and info["stages"] == tinfo["stages"]
     assert info["tau_reached"] == tinfo["tau_reached"]
+
+
+@pytest.mark.parametrize("name,N,acc", [("c4", (12, 10, 12, 10, 12, 10), "medium"), ("c4", (9, 10, 8, 10, 12, 10), "low"),
+                                        ("c3", (10, 9, 12, 9, 8), "medium"), ("c2", (14, 12, 12, 16), "low")])
+@pytest.mark.parametrize("comm", [False, True])
+def test_split_pass1_overlap_path_is_bitwise(name, N, acc, comm, monkeypatch):
+    # with >1 rank, pass 1 runs on the interior axis-0 planes while the halo exchange is
+    # in flight on a side stream, then on the boundary planes; ODP_SPLIT_PASS1=1 forces that path on
+    # one rank (without and with the 1-rank communicator) -- same result bit for bit
+    import torch
+    import paper_2204_05520_b200 as odp
+    from paper_2204_05520_b200 import dist as odist
+    w = coarsened(CONFIGS[name], N, tau=(0.0, 0.05, 0.1))
+    w = w.__class__(**{**w.__dict__, "accuracy": acc, "cfl": 0.8 if acc == "low" else 0.5})
+    V0 = torch.from_numpy(make_v0(w, seed=3)).cuda()
+    ref, rinfo = odp.solve_workload(w, V0, kernel="march")
+    monkeypatch.setenv("ODP_SPLIT_PASS1", "1")
+    if comm:
+        g = odist.partitioned_grid(w, 0, 1, torch.cuda.current_device(), force_comm=True)
+        out, info = odp.hj_solve(g, w.dynamics, w.params, V0, w.tau, w.accuracy, w.mode, cfl=w.cfl, kernel="march")
+        n_split = g.launch_count()
+        monkeypatch.setenv("ODP_SPLIT_PASS1", "0")
+        odp.hj_solve(g, w.dynamics, w.params, V0, w.tau, w.accuracy, w.mode, cfl=w.cfl, kernel="march")
+        assert n_split > g.launch_count()          # the split path ran (one extra pass-1 launch per stage)
+        monkeypatch.setenv("ODP_SPLIT_PASS1", "1")
+        g.close()
+    else:
+        out, info = odp.solve_workload(w, V0, kernel="march")
+    torch.cuda.synchronize()
+    assert info["steps"] == rinfo["steps"] and info["stages"] == rinfo["stages"]
+    np.testing.assert_array_equal(out.cpu().numpy(), ref.cpu().numpy())
+    # and with per-launch timing (direct launches, both pass-1 launches inside one timed region)
+    out2, info2 = odp.solve_workload(w, V0, kernel="march", timing=True)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out2.cpu().numpy(), ref.cpu().numpy())
+    assert info2["kernel_ms"]["pass1"] > 0
