@@ -192,3 +192,16 @@ def test_ttr_all_periodic_axes(N):
     out, info = _gpu(N, lo, hi, per, "HOLONOMIC_BALL", (1.0, -1.0), V0, eps=1e-7)
     np.testing.assert_allclose(out, ref, atol=_tol(ref), rtol=0)
     assert info["last_change"] <= 1e-7
+
+
+@pytest.mark.parametrize("fill", [1.0, -1.0])
+def test_ttr_degenerate_targets(fill):
+    # no target node: nothing is ever reached (phi stays `big`); every node a target: phi = 0
+    N, per = (14, 13, 12), (0, 0, 1)
+    lo, hi = (-2.0, -2.0, -math.pi), (2.0, 2.0, math.pi)
+    V0 = np.full(N, fill, np.float32)
+    out, info = _gpu(N, lo, hi, per, "DUBINS3D", (1.0, 1.0, -1.0), V0, big=77.0)
+    np.testing.assert_array_equal(out, 77.0 if fill > 0 else 0.0)
+    assert info["iters"] == 1 and info["last_change"] == 0.0
+    ref, sweeps, _ = oracle.ttr_solve(N, lo, hi, 4, "DUBINS3D", (1.0, 1.0, -1.0), V0, big=77.0)
+    np.testing.assert_array_equal(ref, out)
