@@ -93,3 +93,27 @@ def test_ttr_converged_phi_is_a_fixed_point_of_the_update(dyn, prm, n, per):
     assert np.all(phi[V0 <= 0] == 0.0) and np.all(phi >= 0.0)
     again = brute.ttr_boundary_rule(N, per, phi.copy())
     np.testing.assert_allclose(again, phi, atol=1e-12, rtol=0)
+
+
+def test_ttr_2d_box_linf_target_rates():
+    # xdot_i = u_i + d_i, |u_i| <= ubar, |d_i| <= dbar: the minimum time to the square
+    # {max|x_i| <= r} is (max_i |x_i| - r) / (ubar - dbar) (each axis closes independently).  It has
+    # kinks on the diagonals, where a monotone scheme converges at the Crandall-Lions rate h^(1/2) in
+    # the max norm; away from them the rate is >= 1
+    ubar, dbar, r = 1.0, 0.25, 0.5
+    e_all, e_off = [], []
+    for N in (41, 81, 161):
+        x = np.linspace(-2.0, 2.0, N)
+        X, Y = np.meshgrid(x, x, indexing="ij")
+        M = np.maximum(np.abs(X), np.abs(Y))
+        phi, _, change = oracle.ttr_solve((N, N), (-2.0, -2.0), (2.0, 2.0), 0, "HOLONOMIC_BOX", (ubar, dbar, -1.0),
+                                          (M - r).astype(np.float32), eps=1e-10)
+        err = np.abs(phi - np.maximum(M - r, 0.0) / (ubar - dbar))
+        band = (M > 0.7) & (M < 1.8)
+        e_all.append(float(err[band].max()))
+        e_off.append(float(err[band & (np.abs(np.abs(X) - np.abs(Y)) > 0.3)].max()))
+        assert change <= 1e-10
+    r_all = [math.log2(e_all[k] / e_all[k + 1]) for k in range(2)]
+    r_off = [math.log2(e_off[k] / e_off[k + 1]) for k in range(2)]
+    assert all(0.4 <= q <= 0.7 for q in r_all), (e_all, r_all)
+    assert min(r_off) >= 1.0, (e_off, r_off)
