@@ -300,19 +300,27 @@ def ttr_boundary_rule(N, periodic, phi):
     return phi
 
 
-def ttr_jacobi(N, lo, hi, periodic, dyn, params, V0, eps=1e-12, max_iter=200000, big=100.0):
-    """Independent NumPy formulation of the time-to-reach iteration (Alg. 3, readings A31-A34):
-    Jacobi iterations (all nodes from the previous iterate) of ttr_update_map, then the boundary
-    rule.  Its fixed point equals the oracle's Gauss-Seidel one where the boundary rule's min
-    never binds on a non-monotone path (holonomic cases); see test_oracle_ttr."""
+def ttr_jacobi(N, lo, hi, periodic, dyn, params, V0, eps=1e-12, max_iter=200000, big=100.0, order="jacobi"):
+    """Independent NumPy formulation of the time-to-reach iteration (Alg. 3, readings A31-A35):
+    order "jacobi": every node from the previous iterate; order "red_black": the nodes with an even
+    index sum first (from the previous iterate), then the odd ones from the updated values (an
+    in-place Gauss-Seidel ordering, reading A35); then the boundary rule.  Its fixed point equals
+    the oracle's Gauss-Seidel one where the boundary rule's min never binds on a non-monotone path
+    (holonomic cases); see test_oracle_ttr."""
     setup = _ttr_setup(N, lo, hi, periodic, dyn, params)
     interior = setup[5]
     target = np.asarray(V0, dtype=np.float32) <= 0
     phi = np.where(target, 0.0, big)
     upd = interior & ~target
+    colour = np.indices(tuple(N)).sum(axis=0) % 2
     for it in range(max_iter):
         old = phi.copy()
-        phi = np.where(upd, np.minimum(ttr_update_map(N, lo, hi, periodic, dyn, params, phi, setup), phi), phi)
+        if order == "jacobi":
+            phi = np.where(upd, np.minimum(ttr_update_map(N, lo, hi, periodic, dyn, params, phi, setup), phi), phi)
+        else:
+            for c in (0, 1):
+                m = upd & (colour == c)
+                phi = np.where(m, np.minimum(ttr_update_map(N, lo, hi, periodic, dyn, params, phi, setup), phi), phi)
         ttr_boundary_rule(N, periodic, phi)
         if np.abs(phi - old).max() <= eps:
             return phi, it + 1

@@ -66,6 +66,9 @@ def test_ttr_gauss_seidel_and_jacobi_share_the_fixed_point(dyn, prm, per):
     assert change <= 1e-13 and sweeps < 20000 and iters < 200000
     np.testing.assert_allclose(phi, ref, atol=1e-9)
     assert np.all(phi[V0 <= 0] == 0.0) and np.all(phi >= 0.0)
+    rb, iters_rb = brute.ttr_jacobi(N, lo, hi, per, dyn, prm, V0, eps=1e-13, order="red_black")
+    np.testing.assert_allclose(rb, ref, atol=1e-9)         # red-black ordering: same fixed point
+    assert iters_rb < iters
 
 
 @pytest.mark.parametrize("dyn,prm,n,per", [("HOLONOMIC_BALL", (1.0, -1.0), 2, (0, 0)),
