@@ -283,6 +283,8 @@ __global__ void __launch_bounds__(256) k_ttr_march(GridDev g, FParams fp, const 
 // neighbours are LDS with constant offsets; axis-0 neighbours stay in registers (vm, vc) and the
 // next plane's centre (vn) comes from the staged tile; middle axes (NDIM >= 4) through L1/L2.
 constexpr int TTR_TX = 32, TTR_TY = 8;
+constexpr int TTR_NPT = 4;                               // nodes per thread along the tile row
+constexpr int TTR_TW = TTR_TX * TTR_NPT;                 // tile width (columns)
 
 template <class F, int NDIM>
 __global__ void __launch_bounds__(TTR_TX * TTR_TY) k_ttr_tile(GridDev g, FParams fp, const float *__restrict__ src,
@@ -290,7 +292,7 @@ __global__ void __launch_bounds__(TTR_TX * TTR_TY) k_ttr_tile(GridDev g, FParams
                                                               int last_launch, int seg_len, int ntx, int nty) {
     if (st->done) return;
     constexpr int A = NDIM - 2, B = NDIM - 1;            // tile axes (rows, columns)
-    constexpr int SW = TTR_TX + 2, SH = TTR_TY + 2;
+    constexpr int SW = TTR_TW + 2, SH = TTR_TY + 2, U = TTR_NPT;
     __shared__ float tile[3][SH * SW];
     F f;
     {
@@ -314,21 +316,26 @@ __global__ void __launch_bounds__(TTR_TX * TTR_TY) k_ttr_tile(GridDev g, FParams
         mid += (long long)idx[d] * g.stride[d];
     }
     const int tx = threadIdx.x % TTR_TX, ty = threadIdx.x / TTR_TX;
-    const int jb = tcx * TTR_TX + tx, ja = tcy * TTR_TY + ty;    // this thread's node in the plane
-    idx[A] = ja; idx[B] = jb;
-    const bool inside = ja < NA && jb < NB;
-    bool face = !inside;
-    if (inside) {
+    const int ja = tcy * TTR_TY + ty;
+    idx[A] = ja;
+    bool rowface = false;                                // on a non-periodic face of axes 1 .. n-2
 #pragma unroll
-        for (int d = 1; d < NDIM; ++d) face |= !g.per[d] && (idx[d] == 0 || idx[d] == g.N[d] - 1);
+    for (int d = 1; d < B; ++d) rowface |= !g.per[d] && (idx[d] == 0 || idx[d] == g.N[d] - 1);
+    // this thread's U nodes: columns tcx TW + u TX + tx (lanes stay consecutive per node slot)
+    bool inside[U], face[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int jb = tcx * TTR_TW + u * TTR_TX + tx;
+        inside[u] = ja < NA && jb < NB;
+        face[u] = !inside[u] || rowface || (!g.per[B] && (jb == 0 || jb == NB - 1));
     }
     const long long s0 = g.stride[0];
     const int sA = (int)g.stride[A];
     const int a0 = blockIdx.y * seg_len, a1 = min(N0, a0 + seg_len);
     const bool per0 = g.per[0] != 0;
-    // tile loader: this thread's (at most 2) tile elements, in-plane offsets fixed per CTA (halo
-    // wrapped on periodic axes, clamped on the others: those values are only read by face nodes,
-    // which are not updated here); cp.async into a 3-stage ring, one commit group per plane
+    // tile loader: this thread's tile elements, in-plane offsets fixed per CTA (halo wrapped on
+    // periodic axes, clamped on the others: those values are only read by face nodes, which are not
+    // updated here); cp.async into a 3-stage ring, one commit group per plane
     constexpr int NT = TTR_TX * TTR_TY, NE = (SH * SW + NT - 1) / NT;
     int eoff[NE];
     bool eok[NE];
@@ -337,7 +344,7 @@ __global__ void __launch_bounds__(TTR_TX * TTR_TY) k_ttr_tile(GridDev g, FParams
         const int e = threadIdx.x + k * NT;
         eok[k] = e < SH * SW;
         const int r = e / SW, cc = e - r * SW;
-        int ga = tcy * TTR_TY + r - 1, gb = tcx * TTR_TX + cc - 1;
+        int ga = tcy * TTR_TY + r - 1, gb = tcx * TTR_TW + cc - 1;
         if (g.per[A]) ga = ga < 0 ? ga + NA : (ga >= NA ? ga - NA : ga); else ga = max(0, min(NA - 1, ga));
         if (g.per[B]) gb = gb < 0 ? gb + NB : (gb >= NB ? gb - NB : gb); else gb = max(0, min(NB - 1, gb));
         eoff[k] = ga * sA + gb;
@@ -357,16 +364,22 @@ __global__ void __launch_bounds__(TTR_TX * TTR_TY) k_ttr_tile(GridDev g, FParams
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     auto plane = [&](int i0) -> const float * { return src + (long long)at0(i0) * s0 + mid; };
-    Pt q;
-    if (inside) {
+    Pt q[U];
 #pragma unroll
-        for (int d = 1; d < NDIM; ++d) load_axis<F>(g, q, d, idx[d]);
-    }
-    const uint32_t ctr4 = 4u * (uint32_t)((ty + 1) * SW + tx + 1);
-    const long long me = mid + (long long)ja * sA + jb;  // in-plane element of this thread's node
+    for (int u = 0; u < U; ++u)
+        if (inside[u]) {
+#pragma unroll
+            for (int d = 1; d < B; ++d) load_axis<F>(g, q[u], d, idx[d]);
+            load_axis<F>(g, q[u], B, tcx * TTR_TW + u * TTR_TX + tx);
+        }
+    const long long me = mid + (long long)ja * sA + tcx * TTR_TW + tx;   // element of node slot 0
     float cmax = 0.f;
-    float vm = 0.f, vc = 0.f;
-    if (inside) vm = fabsf(src[(long long)at0(a0 - 1) * s0 + me]);
+    float vm[U], vc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        vm[u] = 0.f; vc[u] = 0.f;
+        if (inside[u]) vm[u] = fabsf(src[(long long)at0(a0 - 1) * s0 + me + u * TTR_TX]);
+    }
     uint32_t sc = tb0, sn = tb0 + TB, sf = tb0 + 2 * TB;   // stages: plane i0, i0 + 1, i0 + 2
     issue(sc, plane(a0));
     issue(sn, plane(a0 + 1));
@@ -377,26 +390,31 @@ __global__ void __launch_bounds__(TTR_TX * TTR_TY) k_ttr_tile(GridDev g, FParams
         asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
         return v;
     };
+    const uint32_t ctr0 = 4u * (uint32_t)((ty + 1) * SW + tx + 1);
     for (int i0 = a0; i0 < a1; ++i0, dp += s0) {
         issue(sf, pf);                                   // (a group is committed even past the segment)
         pf = (i0 + 3 < N0) ? pf + s0 : plane(i0 + 3);
         asm volatile("cp.async.wait_group 1;" ::: "memory");   // planes i0 and i0 + 1 have landed
         __syncthreads();
-        if (inside) {
-            if (i0 == a0) vc = ld(sc + ctr4);
-            const float vn = ld(sn + ctr4);
-            const float old = vc;
+        const bool face0 = !per0 && (i0 == 0 || i0 == N0 - 1);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (!inside[u]) continue;
+            const uint32_t c4 = ctr0 + 4u * (uint32_t)(u * TTR_TX);
+            if (i0 == a0) vc[u] = ld(sc + c4);
+            const float vn = ld(sn + c4);
+            const float old = vc[u];
             float v = old;
-            if (!face && !is_target(old) && (per0 || (i0 != 0 && i0 != N0 - 1))) {
-                load_axis<F>(g, q, 0, i0);
+            if (!face[u] && !face0 && !is_target(old)) {
+                load_axis<F>(g, q[u], 0, i0);
                 float p[NDIM];
                 float num = 0.f, den = 0.f;
 #pragma unroll
                 for (int d = 0; d < NDIM; ++d) {
                     float vp, vmd;
-                    if (d == 0) { vp = fabsf(vn); vmd = vm; }
-                    else if (d == A) { vp = fabsf(ld(sc + ctr4 + 4u * SW)); vmd = fabsf(ld(sc + ctr4 - 4u * SW)); }
-                    else if (d == B) { vp = fabsf(ld(sc + ctr4 + 4u)); vmd = fabsf(ld(sc + ctr4 - 4u)); }
+                    if (d == 0) { vp = fabsf(vn); vmd = vm[u]; }
+                    else if (d == A) { vp = fabsf(ld(sc + c4 + 4u * SW)); vmd = fabsf(ld(sc + c4 - 4u * SW)); }
+                    else if (d == B) { vp = fabsf(ld(sc + c4 + 4u)); vmd = fabsf(ld(sc + c4 - 4u)); }
                     else {
                         const long long sd = g.stride[d];
                         long long op = sd, om = -sd;
@@ -404,22 +422,22 @@ __global__ void __launch_bounds__(TTR_TX * TTR_TY) k_ttr_tile(GridDev g, FParams
                             if (idx[d] == g.N[d] - 1) op = -(long long)(g.N[d] - 1) * sd;
                             if (idx[d] == 0) om = (long long)(g.N[d] - 1) * sd;
                         }
-                        const float *pc = src + (dp - dst);
+                        const float *pc = src + (dp - dst) + u * TTR_TX;
                         vp = fabsf(pc[op]); vmd = fabsf(pc[om]);
                     }
                     p[d] = (vp - vmd) * g.hih[d];        // central difference (A32)
-                    const float a = f.alpha(d, q);
+                    const float a = f.alpha(d, q[u]);
                     num = fmaf(a * g.hih[d], vp + vmd, num);
                     den = fmaf(a, g.inv_dx[d], den);
                 }
-                const float H = -f.ham(q, p) - 1.f;      // A32: H_TTR = -H_reach(goal -1) - 1
+                const float H = -f.ham(q[u], p) - 1.f;   // A32: H_TTR = -H_reach(goal -1) - 1
                 const float nv = den > 0.f ? (num - H) / den : old;   // l.10-11 (A33)
                 v = fminf(nv, old) + 0.f;                // l.12
                 cmax = fmaxf(cmax, fabsf(v - old));
             }
-            *dp = v;                                     // (A34: target / faces keep their value)
-            vm = fabsf(vc);
-            vc = vn;
+            dp[u * TTR_TX] = v;                          // (A34: target / faces keep their value)
+            vm[u] = fabsf(vc[u]);
+            vc[u] = vn;
         }
         __syncthreads();                                 // stage sc is refilled by the next issue
         const uint32_t t = sc; sc = sn; sn = sf; sf = t;

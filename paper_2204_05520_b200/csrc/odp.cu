@@ -1316,7 +1316,7 @@ static odp_status ttr_device(odp_grid *g, int dyn, const double *params, int npa
     int ntx = 1, nty = 1, tile_seg = 1;
     dim3 grid_tile(1, 1);
     if (use_tile) {
-        ntx = (int)((g->N[n - 1] + TTR_TX - 1) / TTR_TX);
+        ntx = (int)((g->N[n - 1] + TTR_TW - 1) / TTR_TW);
         nty = (int)((g->N[n - 2] + TTR_TY - 1) / TTR_TY);
         long long nb = (long long)ntx * nty;
         for (int d = 1; d < n - 2; ++d) nb *= g->N[d];
