@@ -205,3 +205,17 @@ def test_ttr_degenerate_targets(fill):
     assert info["iters"] == 1 and info["last_change"] == 0.0
     ref, sweeps, _ = oracle.ttr_solve(N, lo, hi, 4, "DUBINS3D", (1.0, 1.0, -1.0), V0, big=77.0)
     np.testing.assert_array_equal(ref, out)
+
+
+@pytest.mark.parametrize("dyn,prm,per,N", [c for c in CASES if len(c[3]) >= 3][:4])
+def test_ttr_column_march_fallback_matches(dyn, prm, per, N, monkeypatch):
+    # ODP_TTR_TILE=0: the column-marching kernel (the NDIM = 2 path) on the 3D+ cases
+    monkeypatch.setenv("ODP_TTR_TILE", "0")
+    n = len(N)
+    lo, hi = _coords(dyn, per, N)
+    axes = [axis_nodes(N[d], lo[d], hi[d], bool(per[d])) for d in range(n)]
+    X = np.meshgrid(*axes, indexing="ij")
+    V0 = (np.sqrt(X[0] ** 2 + X[1] ** 2) - 1.0 + 0.05 * np.random.default_rng(7).uniform(-1, 1, N)).astype(np.float32)
+    ref, _ = brute.ttr_jacobi(N, lo, hi, per, dyn, prm, V0, eps=1e-12)
+    out, info = _gpu(N, lo, hi, per, dyn, prm, V0, eps=1e-7)
+    np.testing.assert_allclose(out, ref, atol=_tol(ref), rtol=0)
