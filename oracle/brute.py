@@ -381,7 +381,8 @@ def vi_successors(N, lo, hi, periodic, model, params):
             flat = np.zeros(tuple(N), np.int64)
             for d in range(n):
                 q = (delta[d] * inv_dx[d]).astype(f32)
-                j = I[d] + np.rint(q).astype(np.int64)
+                fl = np.floor(q)                       # nearest node, ties toward the larger index
+                j = I[d] + (fl + ((q - fl) >= f32(0.5))).astype(np.int64)
                 j = np.mod(j, N[d]) if periodic[d] else np.clip(j, 0, N[d] - 1)
                 flat = flat + j * strides[d]
             row.append(flat.ravel())

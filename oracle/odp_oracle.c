@@ -749,7 +749,7 @@ int oracle_ttr_solve(int n, const int64_t *N, const double *lo, const double *hi
  * nearest-neighbour successor of the note under it.  Readings:
  *   A36 the MDP: S = the grid's nodes; a model gives a finite action set, K outcomes per action
  *       with probabilities p_k and displacements Delta(s, a, k); s' = the node nearest to
- *       s + Delta: per axis i' = i + rint(Delta_d / dx_d) computed in FLOAT32 (the kernel's
+ *       s + Delta: per axis i' = i + round_half_up(Delta_d / dx_d) computed in FLOAT32 (the kernel's
  *       precision: an integer decided by floating point), wrapped on periodic axes, clamped to
  *       [0, N-1] on the others.  Models:
  *         MDP_HOLONOMIC [speed, dt, gamma]: actions {stay, +-e_d}, Delta = +-dt speed e_d, K = 1.
@@ -807,6 +807,15 @@ static int omdp_init(omdp *m, int model, int n, const double *prm, int np) {
 }
 
 /* flat index of the successor of node idx under (a, k) -- A36 (float32 decision) */
+
+/* nearest node along an axis for a displacement of q cells, in float32: round half up, i.e. ties
+ * toward the larger index (SPEC nearest_index); q - floor(q) is exact in float32 */
+static int64_t nearest_shift_f32(float q) {
+    const float fl = floorf(q);
+    const float fr = q - fl;
+    return (int64_t)fl + (fr >= 0.5f ? 1 : 0);
+}
+
 static int64_t omdp_succ(const og *g, const omdp *m, const float *inv_dx, const int64_t *idx, int a, int k) {
     float delta[6] = {0};
     if (m->model == OR_MDP_HOLONOMIC) {
@@ -824,7 +833,7 @@ static int64_t omdp_succ(const og *g, const omdp *m, const float *inv_dx, const 
     int64_t flat = 0;
     for (int d = 0; d < g->n; ++d) {
         const float q = delta[d] * inv_dx[d];
-        int64_t j = idx[d] + (int64_t)rintf(q);
+        int64_t j = idx[d] + nearest_shift_f32(q);
         if (g->per[d]) { j %= g->N[d]; if (j < 0) j += g->N[d]; }
         else j = j < 0 ? 0 : (j > g->N[d] - 1 ? g->N[d] - 1 : j);
         flat += j * g->stride[d];

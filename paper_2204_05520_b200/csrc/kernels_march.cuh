@@ -284,7 +284,7 @@ struct MarchArgs {
     int sn[3];            // local extents of the side axes (work order, march_col)
     int b1;               // axis-1 block of the work order (divides sn[1])
     int ncols;            // columns (product of the side extents)
-    int dbg;              // experiments only (ODP_MARCH_DBG): 2 = skip the arithmetic, 4 = skip the copies
+    int dbg;              // 0 in the production build; ODP_MARCH_DBG under -DODP_MARCH_EXPERIMENTS only
     int K, nseg, units;   // marching segment length, segments per column, work units
     // axis-0 subset of the columns (multi-GPU overlap): 0 all, 1 interior planes
     // [i0r, N0 - i0r), 2 boundary planes [0, i0r) and [N0 - i0r, N0); s0n = planes in the subset
@@ -1050,7 +1050,9 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     if (cols_rb * a.nseg > (1LL << 31) - 1) return false;
     a.units = (int)(cols_rb * a.nseg);
     a.dbg = 0;
+#ifdef ODP_MARCH_EXPERIMENTS       // timing experiments only: never in the production build (wrong results)
     if (const char *env = getenv("ODP_MARCH_DBG")) a.dbg = atoi(env);
+#endif
     a.i0map = 0; a.i0r = 0; a.s0n = a.sn[0];
     a.wslot = 0;                                    // pass 2 launches use slot 1 (march_pass2)
     p->block = ((a.nthr + 31) / 32) * 32 + 32;      // compute warps + the producer warp

@@ -345,8 +345,10 @@ __global__ void __launch_bounds__(TTR_TX * TTR_TY) k_ttr_tile(GridDev g, FParams
         eok[k] = e < SH * SW;
         const int r = e / SW, cc = e - r * SW;
         int ga = tcy * TTR_TY + r - 1, gb = tcx * TTR_TW + cc - 1;
-        if (g.per[A]) ga = ga < 0 ? ga + NA : (ga >= NA ? ga - NA : ga); else ga = max(0, min(NA - 1, ga));
-        if (g.per[B]) gb = gb < 0 ? gb + NB : (gb >= NB ? gb - NB : gb); else gb = max(0, min(NB - 1, gb));
+        // full modulo on periodic axes: the tile (TW + 2 columns, TY + 2 rows) can reach more than
+        // one period past the face when the extent is small (e.g. a 12-node theta axis)
+        if (g.per[A]) ga = ((ga % NA) + NA) % NA; else ga = max(0, min(NA - 1, ga));
+        if (g.per[B]) gb = ((gb % NB) + NB) % NB; else gb = max(0, min(NB - 1, gb));
         eoff[k] = ga * sA + gb;
     }
     auto at0 = [&](int i0) -> int {                      // wrapped / clamped plane index

@@ -24,6 +24,13 @@ struct MdpParams {
     float gamma;
 };
 
+// Index shift of the nearest node for a displacement of q cells: ties toward the larger index
+// (nearest_index, "round half up", S:65 / S:81).  q - floor(q) is exact in float32.
+__device__ __forceinline__ int nearest_shift(float q) {
+    const float fl = floorf(q);
+    return (int)fl + (__fsub_rn(q, fl) >= 0.5f ? 1 : 0);
+}
+
 // Displacement Delta(s, a, k) in float32 with every product and sum rounded separately (no FMA
 // contraction: the snapped node is an integer decided by float arithmetic, A36).
 template <int NDIM>
@@ -98,13 +105,13 @@ __global__ void __launch_bounds__(256) k_vi_march(GridDev g, MdpParams mp, const
                 int o = 0;
 #pragma unroll
                 for (int d = 1; d < NDIM; ++d) {
-                    int j = idx[d] + (int)rintf(__fmul_rn(dl[d], g.inv_dx[d]));
+                    int j = idx[d] + nearest_shift(__fmul_rn(dl[d], g.inv_dx[d]));
                     if (g.per[d]) { j %= g.N[d]; if (j < 0) j += g.N[d]; }
                     else j = max(0, min(g.N[d] - 1, j));
                     o += (j - idx[d]) * (int)g.stride[d];
                 }
                 off[a * M::K + k] = o;
-                sh0[a * M::K + k] = (int)rintf(__fmul_rn(dl[0], g.inv_dx[0]));
+                sh0[a * M::K + k] = nearest_shift(__fmul_rn(dl[0], g.inv_dx[0]));
             }
         const bool per0 = g.per[0] != 0;
         const long long s0 = ncol;

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdarg>
+#include <cstdint>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -489,6 +490,7 @@ struct odp_grid {
     cudaStream_t own_stream = nullptr;
     cudaStream_t side_stream = nullptr;     // NCCL halo exchange overlapped with interior pass 1
     cudaEvent_t ev_in = nullptr, ev_halo = nullptr;
+    cudaEvent_t ev_join[2] = {nullptr, nullptr};   // NULL-stream callers: order own_stream after / before the legacy stream
     std::vector<cudaEvent_t> events;
     long long launches = 0;
     float *d_stage = nullptr;     // staging buffers of the *_host entry points (grown on demand)
@@ -517,6 +519,7 @@ static void free_device(odp_grid *g) {
     if (g->side_stream) cudaStreamDestroy(g->side_stream);
     if (g->ev_in) cudaEventDestroy(g->ev_in);
     if (g->ev_halo) cudaEventDestroy(g->ev_halo);
+    for (auto &e : g->ev_join) { if (e) cudaEventDestroy(e); e = nullptr; }
     g->side_stream = nullptr; g->ev_in = nullptr; g->ev_halo = nullptr;
     for (auto e : g->events) cudaEventDestroy(e);
     g->events.clear();
@@ -545,6 +548,7 @@ extern "C" odp_status odp_grid_create(int dims, const double *lo, const double *
         g->N[d] = N[d]; g->lo[d] = lo[d]; g->hi[d] = hi[d];
         g->per[d] = (periodic_mask >> d) & 1u;
         g->dx[d] = g->per[d] ? (hi[d] - lo[d]) / (double)N[d] : (hi[d] - lo[d]) / (double)(N[d] - 1);   // A15
+        if (g->P > INT64_MAX / N[d]) { delete g; return fail(ODP_EINVAL, "point count overflows int64 at axis %d", d); }
         g->P *= N[d];
     }
     if (dims > 1 && g->P / g->N[0] > ((int64_t)1 << 31) - 1) { delete g; return fail(ODP_EINVAL, "axis-0 plane exceeds 2^31 points"); }
@@ -663,6 +667,7 @@ static odp_status ensure_device(odp_grid *g, int nparts_needed) {
         CUDA_TRY(cudaMalloc(&g->d_state, sizeof(DevState)));
         CUDA_TRY(cudaMallocHost(&g->h_state, sizeof(DevState)));
         CUDA_TRY(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
+        for (auto &e : g->ev_join) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     if (!g->d_buf[0]) {
         g->halo_elems = R_MAX * plane;
@@ -696,6 +701,29 @@ static odp_status stage_buffer(odp_grid *g, size_t elems, float **out) {
     *out = g->d_stage;
     return ODP_OK;
 }
+
+// The stream a call runs on.  A NULL opts->stream (torch's legacy default stream reports handle 0)
+// means "the caller's default stream": the call then runs on the handle's own non-blocking stream,
+// ordered AFTER everything already enqueued on the legacy default stream (the caller may have just
+// produced V0 / target / R there) and, on exit, the legacy stream is ordered after the call (the
+// caller may reuse the output memory at once).  An explicit stream is used as given.
+struct StreamScope {
+    cudaStream_t s = nullptr, legacy_join = nullptr;
+    cudaEvent_t done = nullptr;
+    StreamScope(odp_grid *g, void *user) {
+        if (user) { s = (cudaStream_t)user; return; }
+        s = g->own_stream;
+        cudaEventRecord(g->ev_join[0], cudaStreamLegacy);
+        cudaStreamWaitEvent(s, g->ev_join[0], 0);
+        legacy_join = s;
+        done = g->ev_join[1];
+    }
+    ~StreamScope() {
+        if (!legacy_join) return;
+        cudaEventRecord(done, legacy_join);
+        cudaStreamWaitEvent(cudaStreamLegacy, done, 0);
+    }
+};
 
 static GridDev make_griddev(const odp_grid *g) {
     GridDev d;
@@ -857,7 +885,8 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
     }
     const int nparts1 = split ? 2 * mp.grid : nparts;      // pass-1 partial records (launch_fin)
 
-    cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
+    StreamScope sscope(g, opts ? opts->stream : nullptr);
+    cudaStream_t s = sscope.s;
     const double cfl = (opts && opts->cfl > 0.0) ? opts->cfl : (accuracy == ODP_LOW ? 0.8 : 0.5);   // A7
     const double eps = 1e-12 * std::max(1.0, tau[ntau - 1]);
     const int brt = mode == ODP_BRT;
@@ -1146,7 +1175,8 @@ extern "C" odp_status odp_hj_solve_host(odp_grid *g, int dynamics_id, const doub
     if ((st = ensure_device(g, 1))) return st;
     const int nout = (opts && opts->write_initial) ? ntau : ntau - 1;
     const size_t P = (size_t)local_points(g), bytes = P * sizeof(float);
-    cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
+    StreamScope sscope(g, opts ? opts->stream : nullptr);
+    cudaStream_t s = sscope.s;
     const bool has_t = opts && opts->target;
     float *base = nullptr;
     if ((st = stage_buffer(g, P * (size_t)(1 + nout + (has_t ? 1 : 0)), &base))) return st;
@@ -1292,7 +1322,8 @@ static odp_status ttr_device(odp_grid *g, int dyn, const double *params, int npa
         CUDA_TRY(cudaMalloc(&g->d_ttr, sizeof(TtrState)));
         CUDA_TRY(cudaMallocHost(&g->h_ttr, sizeof(TtrState)));
     }
-    cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
+    StreamScope sscope(g, opts ? opts->stream : nullptr);
+    cudaStream_t s = sscope.s;
     const int n = g->n;
     const TtrFns fn = ttr_select(dyn, n);
     GridDev gd = make_griddev(g);
@@ -1391,7 +1422,8 @@ extern "C" odp_status odp_ttr_solve_host(odp_grid *g, int dynamics_id, const dou
     if (!V0 || !phi) return fail(ODP_EINVAL, "NULL V0/phi");
     if ((st = ensure_device(g, 1))) return st;
     const size_t bytes = (size_t)local_points(g) * sizeof(float);
-    cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
+    StreamScope sscope(g, opts ? opts->stream : nullptr);
+    cudaStream_t s = sscope.s;
     float *dV0 = nullptr, *dphi = nullptr;
     if ((st = stage_buffer(g, 2 * (size_t)local_points(g), &dV0))) return st;
     dphi = dV0 + local_points(g);
@@ -1437,7 +1469,8 @@ static odp_status vi_device(odp_grid *g, int model, const double *params, int np
         CUDA_TRY(cudaMalloc(&g->d_ttr, sizeof(TtrState)));
         CUDA_TRY(cudaMallocHost(&g->h_ttr, sizeof(TtrState)));
     }
-    cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
+    StreamScope sscope(g, opts ? opts->stream : nullptr);
+    cudaStream_t s = sscope.s;
     MdpParams mp;
     memset(&mp, 0, sizeof mp);
     if (model == ODP_MDP_HOLONOMIC) {
@@ -1505,7 +1538,8 @@ extern "C" odp_status odp_vi_solve_host(odp_grid *g, int model_id, const double 
     odp_status st;
     if ((st = ensure_device(g, 1))) return st;
     const size_t bytes = (size_t)local_points(g) * sizeof(float);
-    cudaStream_t s = (opts && opts->stream) ? (cudaStream_t)opts->stream : g->own_stream;
+    StreamScope sscope(g, opts ? opts->stream : nullptr);
+    cudaStream_t s = sscope.s;
     float *dR = nullptr, *dV = nullptr;
     if ((st = stage_buffer(g, 2 * (size_t)local_points(g), &dR))) return st;
     dV = dR + local_points(g);

@@ -4,7 +4,8 @@
   l.8-10 fires at the first t with r gamma^(t-1) < threshold (geometric series, exact);
 * holonomic one-cell moves, reward 1 on a goal node: V* = gamma^d / (1 - gamma), d the grid (L1,
   wrapped on periodic axes) distance to the goal (shortest path with discount);
-* nearest-node successors: hand-computed shifts (rint ties to even), and the NumPy successor tables;
+* nearest-node successors: hand-computed shifts (ties toward the larger index), the SPEC
+  nearest_index golden example (S:69-70), and the NumPy successor tables;
 * Dubins MDP with slip: Jacobi and in-place orders reach the exact Bellman fixed point computed by
   policy iteration (sparse linear solves) in oracle/brute.py; Jacobi iterates equal NumPy's.
 """
@@ -61,7 +62,7 @@ def test_vi_holonomic_discounted_shortest_path(N, per, goal, order):
 
 
 def test_vi_successor_rounding_and_faces():
-    # x axis: dx = 0.5; dt v = 0.75 -> 1.5 cells -> rint ties to even -> 2; v/2 -> 0.75 cells -> 1
+    # x axis: dx = 0.5; dt v = 0.75 -> 1.5 cells -> tie, toward the larger index -> 2; v/2 -> 0.75 cells -> 1
     N, lo, hi = (9, 5, 8), (0.0, 0.0, -math.pi), (4.0, 2.0, math.pi)
     prm = (0.75, 1.0, 1.0, 0.0, 0.0, 0.9)          # vbar 0.75, wbar 1, dt 1, no slip
     st = [5 * 8, 8, 1]
@@ -131,3 +132,27 @@ def test_vi_holonomic_jacobi_iterates_equal_numpy(N, per):
     for t in (1, 4):
         V, _, _ = oracle.vi_solve(N, lo, hi, pm, "HOLONOMIC", prm, R, threshold=0.0, max_iters=t)
         np.testing.assert_allclose(V, brute.vi_jacobi(N, lo, hi, per, "HOLONOMIC", prm, R, t), atol=1e-13)
+
+
+def test_vi_successor_ties_round_half_up():
+    """SPEC nearest_index ("ties round toward the larger index"; example S:69-70: on the 1D grid
+    [0, 0.25, 0.5, 0.75, 1] the midpoint 0.375 snaps to index 2).  Holonomic moves of exactly half a
+    cell: +e from node 1 lands on 0.375 -> node 2; -e lands on 0.125 -> node 1 (the larger index),
+    where round-half-to-even would pick node 0."""
+    N, lo, hi = (5,), (0.0,), (1.0,)
+    prm = (0.125, 1.0, 0.9)                       # speed * dt = 0.125 = half of dx = 0.25
+    # actions: 0 stay, 1 +e0, 2 -e0
+    assert oracle.vi_successor(N, lo, hi, 0, "HOLONOMIC", prm, (1,), 1, 0) == 2
+    assert oracle.vi_successor(N, lo, hi, 0, "HOLONOMIC", prm, (1,), 2, 0) == 1
+    assert oracle.vi_successor(N, lo, hi, 0, "HOLONOMIC", prm, (0,), 1, 0) == 1
+    assert oracle.vi_successor(N, lo, hi, 0, "HOLONOMIC", prm, (2,), 2, 0) == 2
+    # 2.5 cells -> 3 (half-to-even would give 2), -1.5 cells -> -1 (half-to-even: -2)
+    N, lo, hi = (16,), (0.0,), (15.0,)
+    prm = (2.5, 1.0, 0.9)
+    assert oracle.vi_successor(N, lo, hi, 0, "HOLONOMIC", prm, (5,), 1, 0) == 8
+    assert oracle.vi_successor(N, lo, hi, 0, "HOLONOMIC", prm, (5,), 2, 0) == 3
+    prm = (1.5, 1.0, 0.9)
+    assert oracle.vi_successor(N, lo, hi, 0, "HOLONOMIC", prm, (5,), 2, 0) == 4
+    # the NumPy tables follow the same rule
+    succ = brute.vi_successors(N, lo, hi, (0,), "HOLONOMIC", (2.5, 1.0, 0.9))
+    assert succ[1][0][5] == 8 and succ[2][0][5] == 3
