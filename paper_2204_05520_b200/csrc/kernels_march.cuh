@@ -59,7 +59,7 @@ namespace odp {
 #ifndef ODP_MARCH_SELP
 #define ODP_MARCH_SELP 0       // 1: ENO pick as FSET + 3 FMA-pipe ops instead of FSETP + FSEL
 #endif
-constexpr int MARCH_MAXT1 = 512;   // threads per CTA, NP = 1
+constexpr int MARCH_MAXT1 = 512;   // threads per CTA, NP = 1 (compute warps + the producer warp)
 constexpr int MARCH_MAXT2 = 640;   // threads per CTA, NP = 2
 
 // ---- packed fp32 helpers (FADD2 / FMUL2 / FFMA2 on sm_100a) -------------------------------------
@@ -105,9 +105,13 @@ __device__ __forceinline__ float max3nan(float a, float b, float c) {   // NaN-p
     return r;
 }
 
-// range of the two sides of an edge {d1 - m/2, d1 + m/2} into [mn, mx] (both nodes of a pair)
-__device__ __forceinline__ void inc_edge(float2 m, float2 d1, float &mn, float &mx) {
-    const float2 am = abs2(m);
+// |pick(a, b)| = min(|a|, |b|): the magnitude of the ENO2 selection without the selection itself
+__device__ __forceinline__ float2 amin2(float2 a, float2 b) {
+    return f2(fminf(fabsf(a.x), fabsf(b.x)), fminf(fabsf(a.y), fabsf(b.y)));
+}
+// range of the two sides of an edge {d1 - |m|/2, d1 + |m|/2} into [mn, mx] (both nodes of a pair);
+// am = |m| (pass 1 never needs the sign of the selection)
+__device__ __forceinline__ void inc_edge(float2 am, float2 d1, float &mn, float &mx) {
     const float2 lo = fma2(f2s(-0.5f), am, d1), hi = fma2(f2s(0.5f), am, d1);
     mn = min3f(mn, lo.x, lo.y);
     mx = max3f(mx, hi.x, hi.y);
@@ -128,6 +132,15 @@ __device__ __forceinline__ float2 lds2(uint32_t addr) {
     return v;
 }
 
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {   // non-blocking phase test
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -226,9 +239,29 @@ template <> struct Terms<FCar4D> { static constexpr unsigned LIN = 0x3, ABS = 0x
 template <> struct Terms<FCar5D> { static constexpr unsigned LIN = 0x7, ABS = 0x18; };
 template <> struct Terms<FDoubleInt6D> { static constexpr unsigned LIN = 0x15, ABS = 0x2a; };
 
+// Per axis, with u = hD-, w = hD+ (units of h) and hih = 1/(2h), H_d + dissipation_d is
+//   c (u+w) hih + k |u+w| hih + alpha (w-u) hih          (A3, A2, A6)
+// For an axis with a linear term only and alpha = |c| (PQ) this is 2 hih [min(c,0) u + max(c,0) w];
+// for an |p| term only and alpha = |k| (AB) it is 2 |k| hih (k < 0 ? min(w, -u) : max(w, -u)) -- exact
+// algebra, one accumulator, no separate dissipation sum.  alpha_d = |c| / |k| holds for every such
+// axis of the compiled-in functors (table C-2; an AB axis's switching-costate sign set is never
+// empty).  Axes with both terms (CAR4D x, y: alpha depends on the range) use the general form.
 template <class F>
 __device__ __forceinline__ void axis_terms(const F &f, int d, const Pt &q0, const Pt &q1, float hih, float2 u,
                                            float2 w, float2 &acc, float2 &dis, float2 *pv) {
+    const bool lin = (Terms<F>::LIN >> d) & 1, ab = (Terms<F>::ABS >> d) & 1;
+    if (F::SEPARABLE && !Sep<F>::ball && lin && !ab) {                      // PQ
+        const float c0 = lin_c(f, d, q0), c1 = lin_c(f, d, q1), h2 = 2.f * hih;
+        acc = fma2(f2(fminf(c0, 0.f) * h2, fminf(c1, 0.f) * h2), u, acc);
+        acc = fma2(f2(fmaxf(c0, 0.f) * h2, fmaxf(c1, 0.f) * h2), w, acc);
+        return;
+    }
+    if (F::SEPARABLE && !Sep<F>::ball && ab && !lin) {                      // AB
+        const float k = abs_k(f, d);
+        const float2 v = k < 0.f ? f2(fminf(w.x, -u.x), fminf(w.y, -u.y)) : f2(fmaxf(w.x, -u.x), fmaxf(w.y, -u.y));
+        acc = fma2(f2s(2.f * fabsf(k) * hih), v, acc);
+        return;
+    }
     const float2 s = add2(u, w), t = sub2(w, u);
     if constexpr (!F::SEPARABLE) {
         pv[d] = mul2(s, f2s(hih));                   // p_d = (D- + D+)/2 (A3); H at the end of the node
@@ -236,8 +269,8 @@ __device__ __forceinline__ void axis_terms(const F &f, int d, const Pt &q0, cons
         const float2 sh = mul2(s, f2s(hih));
         acc = fma2(sh, sh, acc);
     } else {
-        if ((Terms<F>::LIN >> d) & 1) acc = fma2(s, f2(lin_c(f, d, q0) * hih, lin_c(f, d, q1) * hih), acc);
-        if ((Terms<F>::ABS >> d) & 1) {
+        if (lin) acc = fma2(s, f2(lin_c(f, d, q0) * hih, lin_c(f, d, q1) * hih), acc);
+        if (ab) {
             const float k = abs_k(f, d) * hih;
             acc = f2(fmaf(fabsf(s.x), k, acc.x), fmaf(fabsf(s.y), k, acc.y));
         }
@@ -308,9 +341,10 @@ __host__ __device__ constexpr int geo_side_off(int R, int N1, int B, int NST) { 
 __host__ __device__ constexpr int geo_bar_off(int R, int N1, int B, int NSS, int NST) {
     return ((geo_side_off(R, N1, B, NST) + NST * NSS * geo_ssz(N1, B)) + 3) / 4 * 4;
 }
-// <= 16 mbarriers (128 B) + copy table: 32 x 8 B offsets + 32 x 4 B sizes + 8 x 4 B ring fields
+// 4 NST <= 16 mbarriers (128 B) + copy table: 32 x 8 B offsets + 32 x 4 B sizes + 8 x 4 B ring fields
+// + unit queue (4 ints) + issued-step records (3 NST <= 12 ints)
 __host__ __device__ constexpr int geo_smem_bytes(int R, int N1, int B, int NSS, int NST) {
-    return geo_bar_off(R, N1, B, NSS, NST) * 4 + 128 + 32 * 8 + 32 * 4 + 8 * 4 + 16;   // + unit queue
+    return geo_bar_off(R, N1, B, NSS, NST) * 4 + 144 + 32 * 8 + 32 * 4 + 8 * 4 + 16 + 52;
 }
 
 struct MarchUnit {
@@ -394,6 +428,7 @@ __global__ void __launch_bounds__(MARCH_MAXT1, ODP_MARCH_MINB1)
 k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, const float *__restrict__ T,
         float *out, float *partials, const DevState *st, FParams fp, int kind, int brt) {
     static_assert(NP == 1, "the march family computes node pairs (VEC = 2)");
+    static_assert(NST >= 2 && NST <= 4, "pipeline depth 2..4 (<= 18 mbarriers, unit queue of NST)");
     // dynamic work distribution: pass 1 takes units from work[0], pass 2 from work[1]; each pass
     // resets the other pass's counter (that launch has completed: same stream)
     unsigned int *wctr = const_cast<unsigned int *>(&st->work[a.wslot]);
@@ -419,9 +454,8 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + a.bar_off);
     // tma[b]:   the copies of a step with parity b landed (producer arrive.expect_tx + bytes)
     // empty[b]: every compute warp is done reading that step's buffers (one arrive per warp)
-    // gh[k]:    the ghost cells of the centre tile in ring slot k are written (producer arrive);
-    //           filled as soon as the tile lands, R steps before it becomes a centre tile
-    uint64_t *tmab = bars, *empty = bars + NST, *gh = bars + 2 * NST, *ubar = bars + 2 * NST + RS;
+    // ubar[q]:  unit-queue entry q is written (producer arrive)
+    uint64_t *tmab = bars, *empty = bars + NST, *ubar = bars + 2 * NST;
 
     float mn[NDIM], mx[NDIM], mabs = 0.f;
 #pragma unroll
@@ -442,9 +476,12 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     const int qc0 = (tid - lrow * QR) * VEC;           // first column of this thread's nodes
     const int toff = RMG + (lrow + R) * N1 + qc0;      // this thread's nodes in a ring slot
     const int sloc = MARCH_SMARG + lrow * N1 + qc0;    // ... in a side slot
-    // left / right column pairs: the tile itself, or the slot's column-ghost table on the faces
-    const int loff = qc0 == 0 ? RGT + (lrow + R) * 4 - toff : -2;
-    const int roff = qc0 + VEC == N1 ? RGT + (lrow + R) * 4 + 2 - toff : VEC;
+    // left / right column pairs: the tile itself (wrapped within the row on a periodic column
+    // axis); on a non-periodic column face the pair's ghost cells are formed in registers (A12)
+    const bool cfirst = qc0 == 0, clast = qc0 + VEC == N1;
+    const int loff = cfirst ? (a.per1 ? N1 - 2 : 0) : -2;
+    const int roff = clast ? (a.per1 ? -(N1 - 2) : 0) : VEC;
+    const bool gfirst = cfirst && !a.per1, glast = clast && !a.per1;
     Pt qcv[VEC];                                       // in-plane column coordinates (pass 2)
     if constexpr (PASS2) {
 #pragma unroll
@@ -474,7 +511,8 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     long long *t_soff = reinterpret_cast<long long *>(smem + a.tab_off);   // [32]
     uint32_t *t_snb = reinterpret_cast<uint32_t *>(t_soff + 32);           // [32] bytes (0 = skip)
     int *t_ring = reinterpret_cast<int *>(t_snb + 32);                      // [8]
-    int *uq = t_ring + 8;                                                   // [2] unit queue (producer -> compute warps)
+    int *uq = t_ring + 8;                                                   // [NST] unit queue (producer -> compute warps)
+    int *prec = uq + 4;                                                     // [3 NST + 1] issued steps: unit, index, first; end marker
     auto make_table = [&](const MarchUnit &U) {
         const int lane = tid & 31;
         int oid[NSA], oN[NSA];
@@ -548,132 +586,67 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
         if (nbw0) tma_bulk_g2s_u32(smem_u32(slot + RMG), W + tt + t_ring[6], nbw0, bar);
         if (nbw1) tma_bulk_g2s_u32(smem_u32(slot + t_ring[5]), W + tt, nbw1, bar);
     };
-    // ghost cells (A12) of the centre tile of a step, in its ring slot: the extrapolated rows
-    // beyond a non-periodic row face, and per owned row the column table [c-2, c-1 | c+N1, c+N1+1]
-    // (extrapolated, or wrapped copies on a periodic column axis)
-    auto fill_ghosts = [&](const MarchUnit &U, int slotk) {
-        const int lane = tid & 31;
-        float *slot = ring + slotk * RSZ;
-        float *row0 = slot + RMG + R * N1;                      // row r0 of the block
-        if (!a.per2) {
-            // rows below 0 (only when the block starts within R of the face) and above N2 - 1;
-            // one lane per column, all ghost rows of that column
-            const bool lo = U.r0 - R < 0, hi = U.r0 + U.nrow + R > N2;
-            if (lo || hi) {
-                for (int c = lane; c < N1; c += 32) {
-                    if (lo) {
-                        const float e = row0[(0 - U.r0) * N1 + c], in = row0[(1 - U.r0) * N1 + c];
-#pragma unroll
-                        for (int k = 1; k <= R; ++k)
-                            if (-k >= U.r0 - R) row0[(-k - U.r0) * N1 + c] = ghost(e, in, (float)k);
-                    }
-                    if (hi) {
-                        const float e = row0[(N2 - 1 - U.r0) * N1 + c], in = row0[(N2 - 2 - U.r0) * N1 + c];
-#pragma unroll
-                        for (int k = 1; k <= R; ++k)
-                            if (N2 - 1 + k < U.r0 + U.nrow + R) row0[(N2 - 1 + k - U.r0) * N1 + c] = ghost(e, in, (float)k);
-                    }
-                }
-            }
-        }
-        // column table: one lane per owned row: [c-2, c-1 | c+N1, c+N1+1]
-        float *gt = slot + RGT + R * 4;                          // table row of block row 0
-        for (int rr = lane; rr < U.nrow; rr += 32) {
-            const float *rowp = row0 + rr * N1;
-            const float2 l = *reinterpret_cast<const float2 *>(rowp);
-            const float2 h = *reinterpret_cast<const float2 *>(rowp + N1 - 2);
-            float4 t;
-            if (a.per1) t = make_float4(h.x, h.y, l.x, l.y);
-            else t = make_float4(ghost(l.x, l.y, 2.f), ghost(l.x, l.y, 1.f), ghost(h.y, h.x, 1.f), ghost(h.y, h.x, 2.f));
-            *reinterpret_cast<float4 *>(gt + rr * 4) = t;
-        }
-    };
-
     if (tid == 0) {
         for (int b = 0; b < NST; ++b) {
             mbar_init(&tmab[b], 1);
             mbar_init(&empty[b], nwc);
+            mbar_init(&ubar[b], 1);
         }
-        for (int k = 0; k < RS; ++k) mbar_init(&gh[k], 1);
-        mbar_init(&ubar[0], 1);
-        mbar_init(&ubar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if ((tid >> 5) == nwc) {
         // ================= producer warp =================
-        // iteration s: (b) once step s-1 is released by every compute warp, issue the copies of
-        //                  step s+1 (the TMA latency overlaps step s);
-        //              (a) when step s's copies have landed, write the ghost cells of the ring
-        //                  tiles that came with them (centre tiles R steps later; at a unit's first
-        //                  step all R+1) and release them (gh)
-        // units are taken from the launch's work counter in order, so the units in flight on the
-        // whole GPU stay a compact range of the L2-friendly work order
+        // Issues the copies of step sn as soon as step sn - NST released its buffers (every compute
+        // warp arrived on empty), i.e. up to NST - 1 steps ahead of the slowest compute warp, and
+        // nothing else: the ghost cells are formed by the compute warps in registers, so the only
+        // serial work per step is the copy issue.  Units come from the launch's work counter in
+        // order and are announced through a queue of NST entries (the units in flight on the whole
+        // GPU stay a compact range of the L2-friendly work order).
+        const int lane = tid & 31;
         int nu = 0;                                          // units announced to the compute warps
         auto grab = [&]() -> int {
             unsigned int v = 0;
-            if ((tid & 31) == 0) v = atomicAdd(wctr, 1u);
+            if (lane == 0) v = atomicAdd(wctr, 1u);
             v = __shfl_sync(0xffffffffu, v, 0);
             const int un = v < (unsigned)a.units ? (int)v : -1;
-            if ((tid & 31) == 0) {
-                uq[nu & 1] = un;
-                mbar_arrive(&ubar[nu & 1]);
+            if (lane == 0) {
+                uq[nu % NST] = un;
+                mbar_arrive(&ubar[nu % NST]);
             }
             ++nu;
             return un;
         };
-        int u = grab();
-        if (u >= 0) {
-        MarchUnit U = march_unit<MA>(a, Nml, mlo, u);
-        int jg = U.m0;
-        bool first = true;                                   // step sp is the first of its unit
-        make_table(U);
-        issue(U, jg, 0, 0);
-        for (int sp = 0;; ++sp) {
-            int jn = jg + 1, un = u;
-            MarchUnit Un = U;
-            const bool fresh = jn >= U.m1;
-            bool more = true;
-            if (fresh) {
-                un = grab();
-                more = un >= 0;
-                if (more) { Un = march_unit<MA>(a, Nml, mlo, un); jn = Un.m0; }
-            }
-            if (more) {
-                const int sr = sp + 1 - NST;             // the step whose buffers step sp + 1 reuses
+        int ui = grab();
+        int sn = 0;
+        while (ui >= 0) {
+            const MarchUnit U = march_unit<MA>(a, Nml, mlo, ui);
+            make_table(U);
+            for (int j = U.m0; j < U.m1; ++j, ++sn) {
+                const int sr = sn - NST;                     // the step whose buffers step sn reuses
                 if (sr >= 0) mbar_wait_sleep(&empty[sr % NST], (uint32_t)((sr / NST) & 1));
-                if (fresh) make_table(Un);
-                issue(Un, jn, sp + 1, fresh ? 0 : R);
+                issue(U, j, sn, j == U.m0 ? 0 : R);
             }
-            mbar_wait_sleep(&tmab[sp % NST], (uint32_t)((sp / NST) & 1));
-#pragma unroll 1
-            for (int k = first ? 0 : R; k <= R; ++k) {
-                if (jg + k >= U.m1) break;
-                if (!(a.dbg & 8)) fill_ghosts(U, (sp + k) % RS);
-                __syncwarp();
-                if ((tid & 31) == 0) mbar_arrive(&gh[(sp + k) % RS]);
-            }
-            if (!more) break;
-            u = un; U = Un; jg = jn; first = fresh;
-        }
+            ui = grab();
         }
     } else {
         // ================= compute warps =================
         int it = 0;                                      // step counter of this CTA (buffer / phase)
-        int rs0 = 0, rph = 0;                            // it % RS (ring slot of the centre tile), (it / RS) & 1
+        int rs0 = 0;                                     // it % RS (ring slot of the centre tile)
         int st0 = 0, sph = 0;                            // it % NST (stage), (it / NST) & 1
         const uint32_t rb_s = smem_u32(ring + toff);    // this thread's nodes in ring slot 0 (bytes)
         const uint32_t sb_s = smem_u32(side + sloc);    // ... in side slot 0 of stage 0
         const uint32_t lof = 4u * (uint32_t)loff, rof = 4u * (uint32_t)roff;
         int rsw = R;                                     // (it + R) % RS: ring slot of the entering window tile
         for (int k = 0;; ++k) {
-            mbar_wait_sleep(&ubar[k & 1], (uint32_t)((k >> 1) & 1));
-            const int u = uq[k & 1];
+            mbar_wait_sleep(&ubar[k % NST], (uint32_t)((k / NST) & 1));
+            const int u = uq[k % NST];
             if (u < 0) break;
             const MarchUnit U = march_unit<MA>(a, Nml, mlo, u);
             const int m0 = U.m0, m1 = U.m1;
             const bool act = lrow < U.nrow && tid < a.nthr;
             const int grow = U.r0 + lrow;                 // global row of this thread
+            const bool rface = !a.per2 && (grow < R || grow > N2 - 1 - R);   // ghost rows in the row window
             int oid[NSA], oN[NSA];
             side_geom(U.col, oid, oN);
             bool oface[NSA];
@@ -731,8 +704,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                         vin = ghost2(e, in, (float)(kin - Nm + 1));
                     }
                 }
-                mbar_wait_sleep(&gh[rs0], (uint32_t)rph);
-                mbar_wait_sleep(&tmab[st0], (uint32_t)sph);
+                mbar_wait_sleep(&tmab[st0], (uint32_t)sph);        // the step's copies landed
                 const uint32_t rcs = rb_s + (uint32_t)(rs0 * RSZ * 4);      // this thread's nodes in the centre tile
                 const uint32_t sbs = sb_s + (uint32_t)(st0 * NSS * SSZ * 4); // ... in side slot 0
 
@@ -775,15 +747,16 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                     // ---- marching axis: carried edge j-1/2, new edge j+1/2 ----
                     if constexpr (R == 2) {
                         const float2 dd1 = d2p(win[0], win[1], win[2]);      // d2_{j+1}
-                        const float2 m = pick2(dd0, dd1);
                         const float2 d1 = sub2(win[1], win[0]);
                         if constexpr (PASS2) {
+                            const float2 m = pick2(dd0, dd1);
                             terms(MA, fma2(f2s(0.5f), mL, dL), fma2(f2s(-0.5f), m, d1));
+                            mL = m;
                         } else {
-                            if (!mper && jg == Nm - 1) inc_val(fma2(f2s(-0.5f), m, d1), mn[MA], mx[MA]);
-                            else inc_edge(m, d1, mn[MA], mx[MA]);
+                            if (!mper && jg == Nm - 1) inc_val(fma2(f2s(-0.5f), pick2(dd0, dd1), d1), mn[MA], mx[MA]);
+                            else inc_edge(amin2(dd0, dd1), d1, mn[MA], mx[MA]);
                         }
-                        dd0 = dd1; mL = m; dL = d1;
+                        dd0 = dd1; dL = d1;
                     } else {
                         const float2 d1 = sub2(win[1], win[0]);
                         if constexpr (PASS2) terms(MA, dL, d1);
@@ -808,7 +781,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                             } else {
                                 inc_val(uu, mn[o], mx[o]);
                                 inc_val(ww, mn[o], mx[o]);
-                                if (R == 2 && oid[o] + 1 <= oN[o] - 1) inc_val(fma2(f2s(0.5f), mr, d1r), mn[o], mx[o]);
+                                if (R == 2 && oid[o] + 1 <= oN[o] - 1) inc_val(fma2(f2s(0.5f), mr, d1r), mn[o], mx[o]);   // D-_{i+1}
                             }
                         } else {
                             // pass 1, interior: the node's upper edge i+1/2 (both sides)
@@ -816,30 +789,81 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                                 const float2 s1 = lds2(so + (uint32_t)(1 * SSZ * 4));
                                 const float2 s2 = lds2(so + (uint32_t)(2 * SSZ * 4));
                                 const float2 s3 = lds2(so + (uint32_t)(3 * SSZ * 4));
-                                inc_edge(pick2(d2p(s1, v0, s2), d2p(v0, s2, s3)), sub2(s2, v0), mn[o], mx[o]);
+                                inc_edge(amin2(d2p(s1, v0, s2), d2p(v0, s2, s3)), sub2(s2, v0), mn[o], mx[o]);
                             } else {
                                 inc_val(sub2(lds2(so + (uint32_t)(1 * SSZ * 4)), v0), mn[o], mx[o]);
                             }
                         }
                     }
 
-                    // ---- in-plane rows (axis n-2): ghost rows are in the slot ----
+                    // ---- in-plane rows (axis n-2): rows beyond a non-periodic face are ghosts (A12) ----
                     {
                         float2 x[2 * R + 1];
+                        if (!PASS2 && !rface) {
+                            // pass 1, interior row: the node's upper edge r+1/2 (both sides)
+                            const uint32_t rs = (uint32_t)(N1 * 4);
+                            if constexpr (R == 2) {
+                                const float2 s1 = lds2(rcs - rs), s2 = lds2(rcs + rs), s3 = lds2(rcs + 2 * rs);
+                                inc_edge(amin2(d2p(s1, v0, s2), d2p(v0, s2, s3)), sub2(s2, v0), mn[NDIM - 2], mx[NDIM - 2]);
+                            } else {
+                                inc_val(sub2(lds2(rcs + rs), v0), mn[NDIM - 2], mx[NDIM - 2]);
+                            }
+                        } else if (!rface) {
 #pragma unroll
-                        for (int k = -R; k <= R; ++k) x[k + R] = k == 0 ? v0 : lds2(rcs + (uint32_t)(k * N1 * 4));
-                        float2 uu, ww, mr, d1r;
-                        classic(x, uu, ww, mr, d1r);
-                        if constexpr (PASS2) terms(NDIM - 2, uu, ww);
-                        else { inc_val(uu, mn[NDIM - 2], mx[NDIM - 2]); inc_val(ww, mn[NDIM - 2], mx[NDIM - 2]); }
+                            for (int k = -R; k <= R; ++k) x[k + R] = k == 0 ? v0 : lds2(rcs + (uint32_t)(k * N1 * 4));
+                        } else {
+#pragma unroll
+                            for (int k = -R; k <= R; ++k) {
+                                const int rr = min(max(grow + k, 0), N2 - 1) - grow;
+                                x[k + R] = k == 0 ? v0 : lds2(rcs + (uint32_t)(rr * N1 * 4));
+                            }
+                            // ghost rows (A12) from the face row e and the next inner row
+                            if (grow == 0) {
+                                x[R - 1] = ghost2(v0, x[R + 1], 1.f);
+                                if (R == 2) x[0] = ghost2(v0, x[R + 1], 2.f);
+                            } else if (R == 2 && grow == 1) {
+                                x[0] = ghost2(x[1], v0, 1.f);
+                            }
+                            if (grow == N2 - 1) {
+                                x[R + 1] = ghost2(v0, x[R - 1], 1.f);
+                                if (R == 2) x[2 * R] = ghost2(v0, x[R - 1], 2.f);
+                            } else if (R == 2 && grow == N2 - 2) {
+                                x[2 * R] = ghost2(x[3], v0, 1.f);
+                            }
+                        }
+                        if (PASS2 || rface) {
+                            float2 uu, ww, mr, d1r;
+                            classic(x, uu, ww, mr, d1r);
+                            if constexpr (PASS2) {
+                                terms(NDIM - 2, uu, ww);
+                            } else {       // face row: D-, D+ and, below the last row, both sides of edge r+1/2
+                                inc_val(uu, mn[NDIM - 2], mx[NDIM - 2]);
+                                inc_val(ww, mn[NDIM - 2], mx[NDIM - 2]);
+                                if (R == 2 && grow + 1 <= N2 - 1) inc_val(fma2(f2s(0.5f), mr, d1r), mn[NDIM - 2], mx[NDIM - 2]);
+                            }
+                        }
                     }
 
                     // ---- in-plane columns (axis n-1): left / right pairs (tile or ghost table) ----
                     {
-                        const float2 lp = lds2(rcs + lof);
-                        const float2 rp = lds2(rcs + rof);
+                        float2 lp = lds2(rcs + lof);
+                        float2 rp = lds2(rcs + rof);
+                        if (gfirst) lp = f2(ghost(v0.x, v0.y, 2.f), ghost(v0.x, v0.y, 1.f));
+                        if (glast) rp = f2(ghost(v0.y, v0.x, 1.f), ghost(v0.y, v0.x, 2.f));
                         float2 uu, ww;
-                        if constexpr (R == 2) {
+                        if constexpr (!PASS2 && R == 2) {
+                            // edges c+1/2 (both sides) and c+3/2 (both sides, or D+_{c+1} on the last pair
+                            // of a non-periodic row); D-_c on the first pair (the face edge c-1/2)
+                            const float d0 = d2s(lp.y, v0.x, v0.y), d1 = d2s(v0.x, v0.y, rp.x), d2 = d2s(v0.y, rp.x, rp.y);
+                            const float fb = v0.y - v0.x, fc = rp.x - v0.y;
+                            const float2 lo = fma2(f2s(-0.5f), f2(fminf(fabsf(d0), fabsf(d1)), fminf(fabsf(d1), fabsf(d2))), f2(fb, fc));
+                            float2 hi = fma2(f2s(0.5f), f2(fminf(fabsf(d0), fabsf(d1)), fminf(fabsf(d1), fabsf(d2))), f2(fb, fc));
+                            if (glast) hi.y = fmaf(-0.5f, pick1(d1, d2), fc);
+                            float l2 = glast ? hi.y : lo.y;
+                            mn[NDIM - 1] = min3f(mn[NDIM - 1], lo.x, l2);
+                            mx[NDIM - 1] = max3f(mx[NDIM - 1], hi.x, hi.y);
+                            if (gfirst) inc_s(fmaf(0.5f, pick1(d2s(lp.x, lp.y, v0.x), d0), v0.x - lp.y), mn[NDIM - 1], mx[NDIM - 1]);
+                        } else if constexpr (R == 2) {
                             // columns -2 -1 | 0 1 | 2 3 ; second differences at -1 0 1 2 ; edges -1/2, 1/2, 3/2
                             const float dm1 = d2s(lp.x, lp.y, v0.x), d0 = d2s(lp.y, v0.x, v0.y);
                             const float d1 = d2s(v0.x, v0.y, rp.x), d2 = d2s(v0.y, rp.x, rp.y);
@@ -852,7 +876,10 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                             ww = f2(v0.y - v0.x, rp.x - v0.y);
                         }
                         if constexpr (PASS2) terms(NDIM - 1, uu, ww);
-                        else { inc_val(uu, mn[NDIM - 1], mx[NDIM - 1]); inc_val(ww, mn[NDIM - 1], mx[NDIM - 1]); }
+                        else if constexpr (R == 1) {
+                            inc_val(ww, mn[NDIM - 1], mx[NDIM - 1]);          // D+_c, D+_{c+1} (= D-_{c+1}, D-_{c+2})
+                            if (gfirst) inc_s(uu.x, mn[NDIM - 1], mx[NDIM - 1]);   // D-_0
+                        }
                     }
 
                     if constexpr (PASS2) {
@@ -882,7 +909,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                 }
                 __syncwarp();
                 if ((tid & 31) == 0) mbar_arrive(&empty[st0]);   // this warp is done with the step's buffers
-                if (++rs0 == RS) { rs0 = 0; rph ^= 1; }
+                if (++rs0 == RS) rs0 = 0;
                 if (++rsw == RS) rsw = 0;
                 if (++st0 == NST) { st0 = 0; sph ^= 1; }
             }
@@ -915,7 +942,7 @@ struct MarchInst {
     int n1 = 0, b = 0, nst = 2;
     march_fn pass1 = nullptr, pass2 = nullptr;
 };
-constexpr int MARCH_MAX_INST = 6;
+constexpr int MARCH_MAX_INST = 12;
 struct MarchFnsAll {
     march_fn pass1 = nullptr, pass2 = nullptr;   // generic
     MarchInst inst[MARCH_MAX_INST];
@@ -948,15 +975,18 @@ MarchFnsAll march_fns() {
         t.pass1 = k_march<F, NDIM, R, 1, false>;
         t.pass2 = k_march<F, NDIM, R, 1, true>;
         if constexpr (std::is_same<F, FDoubleInt6D>::value) {     // c4 (30^6), c5 (64 x 48^5)
-            march_add<F, NDIM, R, 30, 30>(t);
-            march_add<F, NDIM, R, 48, 16>(t);
-            if constexpr (R == 2) march_add<F, NDIM, R, 30, 30, 3>(t);    // 3-stage pipeline, 1 CTA/SM (experiment)
+            march_add<F, NDIM, R, 30, 30, 2>(t);
+            march_add<F, NDIM, R, 48, 16, 2>(t);
+            if constexpr (R == 1) march_add<F, NDIM, R, 48, 16, 4>(t);   // c5 LOW
         } else if constexpr (std::is_same<F, FCar5D>::value && R == 2) {   // c3
-            march_add<F, NDIM, R, 40, 20>(t);
+            march_add<F, NDIM, R, 40, 20, 2>(t);
+            march_add<F, NDIM, R, 40, 20, 3>(t);
         } else if constexpr (std::is_same<F, FCar4D>::value && R == 1) {   // c2
-            march_add<F, NDIM, R, 60, 15>(t);
+            march_add<F, NDIM, R, 60, 15, 2>(t);
+            march_add<F, NDIM, R, 60, 15, 4>(t);
         } else if constexpr (std::is_same<F, FDubins3D>::value && R == 1) { // c1
-            march_add<F, NDIM, R, 36, 21>(t);
+            march_add<F, NDIM, R, 36, 21, 2>(t);
+            march_add<F, NDIM, R, 36, 21, 3>(t);
         }
     }
     return t;
@@ -979,34 +1009,45 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     // rows per block: among the B (B N1 % 4 == 0 unless B = N2, <= 512 threads) whose shared
     // memory leaves room for 2 CTAs per SM (else 1), the one wasting the fewest rows in the last
     // (ragged) block, the larger on ties
-    int best = 0;
-    int nst = 2;
-    if (const char *env = getenv("ODP_MARCH_NST")) nst = std::min(3, std::max(2, atoi(env)));
+    // rows per block B and pipeline depth NST: the deepest pipeline (NST = 4, 3, 2) of a compiled
+    // instance whose shared memory still leaves room for 2 CTAs per SM; B among those that fit,
+    // the one wasting the fewest rows in the last (ragged) block, the larger on ties.  NST > 2
+    // exists only as shape-specialised instances; the generic instance runs NST = 2.
+    const bool generic_only = getenv("ODP_MARCH_GENERIC") != nullptr;
+    int nst_env = 0, b_env = 0;
+    if (const char *env = getenv("ODP_MARCH_NST")) nst_env = std::min(4, std::max(2, atoi(env)));
+    if (const char *env = getenv("ODP_MARCH_B")) b_env = atoi(env);
     const bool one_cta = getenv("ODP_MARCH_1CTA") != nullptr;
-    for (int pass = one_cta ? 1 : 0; pass < 2 && !best; ++pass) {
-        const int cap = pass == 0 ? 113 * 1024 : 226 * 1024;
-        int best_waste = 1 << 30;
+    auto pick_b = [&](int nst, int cap) {
+        int bb = 0, best_waste = 1 << 30;
         for (int B = std::min(N2, (MARCH_MAXT1 - 32) / QR); B >= 1; --B) {
             if (B != N2 && (B * N1) % 4) continue;
             if (geo_smem_bytes(R, N1, B, NSS, nst) > cap) continue;
             const int waste = ((N2 + B - 1) / B) * B - N2;
-            if (waste < best_waste) { best_waste = waste; best = B; }
+            if (waste < best_waste) { best_waste = waste; bb = B; }
         }
-    }
-    if (const char *env = getenv("ODP_MARCH_B")) {
-        const int B = atoi(env);
-        if (B >= 1 && B <= N2 && B * QR + 32 <= MARCH_MAXT1 && (B == N2 || (B * N1) % 4 == 0)) best = B;
+        if (b_env >= 1 && b_env <= N2 && b_env * QR + 32 <= MARCH_MAXT1 && (b_env == N2 || (b_env * N1) % 4 == 0)) bb = b_env;
+        return bb;
+    };
+    auto has_inst = [&](int B, int nst) {
+        if (generic_only) return nst == 2;
+        for (int i = 0; i < all.ninst; ++i)
+            if (all.inst[i].n1 == N1 && all.inst[i].b == B && all.inst[i].nst == nst) return true;
+        return nst == 2;
+    };
+    int best = 0, nst = 2;
+    for (int pass = one_cta ? 1 : 0; pass < 2 && !best; ++pass) {
+        const int cap = pass == 0 ? 113 * 1024 : 226 * 1024;
+        for (int cand = nst_env ? nst_env : 4; cand >= 2 && !best; --cand) {
+            const int B = pick_b(cand, cap);
+            if (B && has_inst(B, cand)) { best = B; nst = cand; }
+            if (nst_env) break;
+        }
     }
     if (!best) return false;
     fns->pass1 = all.pass1;
     fns->pass2 = all.pass2;
     fns->specialised = 0;
-    const bool generic_only = getenv("ODP_MARCH_GENERIC") != nullptr;
-    if (nst != 2) {             // only shape-specialised instances have a 3-stage pipeline
-        bool found = false;
-        for (int i = 0; i < all.ninst; ++i) found |= all.inst[i].n1 == N1 && all.inst[i].b == best && all.inst[i].nst == nst;
-        if (!found) return false;
-    }
     for (int i = 0; i < all.ninst && !generic_only; ++i)
         if (all.inst[i].n1 == N1 && all.inst[i].b == best && all.inst[i].nst == nst) {
             fns->pass1 = all.inst[i].pass1;
@@ -1027,7 +1068,7 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     a.rmarg = geo_rmarg(R, N1);
     a.side_off = geo_side_off(R, N1, best, nst);
     a.bar_off = geo_bar_off(R, N1, best, NSS, nst);
-    a.tab_off = a.bar_off + 32;
+    a.tab_off = a.bar_off + 36;                     // 2 NST + R + NST + NST <= 18 mbarriers (144 B)
     for (int o = 0; o < 3; ++o) a.sn[o] = o < MA ? g.N[o] : 1;
     a.b1 = 1;
     if (MA == 3) {

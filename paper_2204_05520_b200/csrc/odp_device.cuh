@@ -139,7 +139,7 @@ struct FHoloBall {   // [ubar, goal]: xdot = u, |u|_2 <= ubar
     static constexpr bool RANGE_FREE = false;
     static constexpr bool SEPARABLE = true, DEPS3 = false;
     static constexpr int NEED_X = 0, NEED_TRIG = 0;
-    static __host__ __device__ int deps(int) { return 0; }
+    static constexpr __host__ __device__ int deps(int) { return 0; }
     float kH, a[NDIM];
     __device__ void init(const FParams &P, const float *mn, const float *mx) {
         kH = P.c[1] * P.c[0];
@@ -171,7 +171,7 @@ struct FHoloBox {    // [ubar, dbar, goal]: xdot_i = u_i + d_i
     static constexpr bool RANGE_FREE = true;
     static constexpr bool SEPARABLE = true, DEPS3 = false;
     static constexpr int NEED_X = 0, NEED_TRIG = 0;
-    static __host__ __device__ int deps(int) { return 0; }
+    static constexpr __host__ __device__ int deps(int) { return 0; }
     float kH, a[NDIM];
     __device__ void init(const FParams &P, const float *mn, const float *mx) {
         const float g = P.c[2];
@@ -197,7 +197,7 @@ struct FDubins3D {   // [v, wbar, goal]: (x, y, th) -> (v cos th, v sin th, w)
     static constexpr bool SEPARABLE = true, DEPS3 = false;
     static constexpr int NDIM = 3;
     static constexpr int NEED_X = 0, NEED_TRIG = 1 << 2;
-    static __host__ __device__ int deps(int d) { return d < 2 ? (1 << 2) : 0; }
+    static constexpr __host__ __device__ int deps(int d) { return d < 2 ? (1 << 2) : 0; }
     float v, kw, a2;
     __device__ void init(const FParams &P, const float *mn, const float *mx) {
         v = P.c[0];
@@ -219,7 +219,7 @@ struct FCar4D {      // [abar, wbar, dxbar, dybar, goal]: (x, y, v, th)
     static constexpr bool SEPARABLE = true, DEPS3 = false;
     static constexpr int NDIM = 4;
     static constexpr int NEED_X = 1 << 2, NEED_TRIG = 1 << 3;
-    static __host__ __device__ int deps(int d) { return d < 2 ? ((1 << 2) | (1 << 3)) : 0; }
+    static constexpr __host__ __device__ int deps(int d) { return d < 2 ? ((1 << 2) | (1 << 3)) : 0; }
     float ka, kw, kdx, kdy, a2, a3;
     SignSet Sx, Sy;
     __device__ void init(const FParams &P, const float *mn, const float *mx) {
@@ -253,7 +253,7 @@ struct FCar5D {      // [abar, alphabar, goal]: (x, y, th, v, w)
     static constexpr bool SEPARABLE = true, DEPS3 = false;
     static constexpr int NDIM = 5;
     static constexpr int NEED_X = (1 << 3) | (1 << 4), NEED_TRIG = 1 << 2;
-    static __host__ __device__ int deps(int d) {
+    static constexpr __host__ __device__ int deps(int d) {
         return d < 2 ? ((1 << 2) | (1 << 3)) : (d == 2 ? (1 << 4) : 0);
     }
     float ka, kal, a3, a4;
@@ -285,7 +285,7 @@ struct FDoubleInt6D {  // [ubar, dbar, goal]: (px, vx, py, vy, pz, vz) -> (v_i, 
     static constexpr bool SEPARABLE = true, DEPS3 = false;
     static constexpr int NDIM = 6;
     static constexpr int NEED_X = (1 << 1) | (1 << 3) | (1 << 5), NEED_TRIG = 0;
-    static __host__ __device__ int deps(int d) { return (d & 1) == 0 ? (1 << (d + 1)) : 0; }
+    static constexpr __host__ __device__ int deps(int d) { return (d & 1) == 0 ? (1 << (d + 1)) : 0; }
     float kv, av[3];
     __device__ void init(const FParams &P, const float *mn, const float *mx) {
         const float g = P.c[2];
@@ -313,7 +313,7 @@ struct FPairDubins3D {  // Eq. 7 [va, vb, abar, bbar, goal]: relativ
     static constexpr int NDIM = 3;
     static constexpr int NEED_X = (1 << 0) | (1 << 1), NEED_TRIG = 1 << 2;
     // alpha_d depends on (x, y) through the switching function and on th through the drift
-    static __host__ __device__ int deps(int) { return 0x7; }
+    static constexpr __host__ __device__ int deps(int) { return 0x7; }
     static constexpr bool RANGE_FREE = false;       // the sign set of q = p_x y - p_y x - p_th
     static constexpr bool SEPARABLE = false, DEPS3 = true;
     float va, vb, ka, kb;                            // ka = goal abar, kb = -goal bbar
