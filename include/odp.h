@@ -173,6 +173,26 @@ odp_status odp_grid_partition(odp_grid *g, int rank, int nranks, const void *id1
 odp_status odp_grid_local_extent(const odp_grid *g, int64_t *i0_begin, int64_t *i0_count);
 
 /*
+ * Loopback transport (tests of the multi-rank path with one GPU).  The same slab partition as
+ * odp_grid_partition, but the nranks handles live in ONE process on ONE device, each driven by its
+ * own host thread: halo planes move by device-to-device copies and the range records are reduced by
+ * a max kernel, ordered with stream events and a host barrier per collective (every rank calls the
+ * same collectives in the same order -- the property the NCCL path relies on as well).  No kernel
+ * waits on another rank's kernel, so the handles' solves never deadlock the device.
+ *
+ * odp_loopback_create -- a transport for nranks (1..64) handles; *out owned by the caller.
+ *   ODP_EINVAL, ODP_ENOMEM, ODP_ECUDA (events, the record buffer on the current device).
+ * odp_grid_partition_loopback -- makes `g` rank `rank`'s slab on the transport (the transport must
+ *   outlive the handle's solves).  Errors as odp_grid_partition.
+ * odp_loopback_destroy -- frees the transport (after every handle on it is destroyed or
+ *   re-partitioned).
+ */
+typedef struct odp_loopback odp_loopback;
+odp_status odp_loopback_create(int nranks, odp_loopback **out);
+odp_status odp_grid_partition_loopback(odp_grid *g, int rank, odp_loopback *lb);
+void odp_loopback_destroy(odp_loopback *lb);
+
+/*
  * Time-to-reach: the stationary HJ equation of Eq. 6 for the TTR
  * function phi(z) = min time to reach the target T = {V0 <= 0} (Eq. 5), by the
  * Lax-Friedrichs iteration of Algorithm 3: phi = 0 on T and `big` elsewhere (l.1);

@@ -202,13 +202,15 @@ def coarsened(w: Workload, N: Sequence[int], name: Optional[str] = None, tau=Non
                    tau=tuple(tau) if tau is not None else w.tau)
 
 
-def make_v0(w: Workload, seed: Optional[int] = None, noise: float = 1e-3, i0=None) -> np.ndarray:
+def make_v0(w: Workload, seed: Optional[int] = None, noise: float = 1e-3, i0=None, box=None) -> np.ndarray:
     """Initial value V0 = target signed distance on the nodes, float64 -> float32 (reading A18).
 
     seed=None gives the plain workload; an integer seed adds noise*U(-1,1) from
     numpy.random.default_rng(seed) (the seeded parity variants of SURVEY.md §8(d)).
     i0 = (begin, count) returns only the axis-0 slab [begin, begin + count) -- bitwise the same
     values as slicing the whole array (a multi-GPU rank builds just its own slab).
+    box = [(begin, count) per axis] returns the sub-box -- bitwise the same values as slicing the
+    whole array (the windowed checks of pin Z12 build only the boxes they need; unseeded only).
     """
     axes = [axis_nodes(n, l, h, bool(p)) for n, l, h, p in zip(w.N, w.lo, w.hi, w.periodic)]
     kind = w.target[0]
@@ -217,6 +219,10 @@ def make_v0(w: Workload, seed: Optional[int] = None, noise: float = 1e-3, i0=Non
         b, c = int(i0[0]), int(i0[1])
         axes[0] = axes[0][b:b + c]
         shape = (c,) + tuple(w.N[1:])
+    if box is not None:
+        assert i0 is None and seed is None
+        axes = [ax[int(b):int(b) + int(c)] for ax, (b, c) in zip(axes, box)]
+        shape = tuple(int(c) for _, c in box)
     if kind in ("cylinder", "sphere"):
         _, taxes, radius = w.target
         acc = np.zeros((1,) * len(shape), dtype=np.float64)

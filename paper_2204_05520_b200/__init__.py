@@ -5,8 +5,8 @@ in include/odp.h (libodp.so, built in-tree).  This package is the thin Python bi
 marshalling only, torch for device memory and streams.  There is no CPU fallback: importing the
 package fails loudly if libodp.so has not been built.
 """
-from .capi import (ACCURACY, DYNAMICS, MODE, Grid, OdpError, comm_unique_id, hj_solve, hj_solve_host,  # noqa: F401
-                   last_error, partition_extent, ttr_solve, ttr_solve_host, version, vi_solve, vi_solve_host)
+from .capi import (ACCURACY, DYNAMICS, MODE, Grid, Loopback, OdpError, comm_unique_id, hj_solve,  # noqa: F401
+                   hj_solve_host, last_error, partition_extent, ttr_solve, ttr_solve_host, version, vi_solve, vi_solve_host)
 
 
 def solve_workload(w, V0, **kw):

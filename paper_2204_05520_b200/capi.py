@@ -25,7 +25,8 @@ DYNAMICS = {"HOLONOMIC_BALL": 0, "HOLONOMIC_BOX": 1, "DUBINS3D": 2, "CAR4D": 3, 
 EXPORTS = ("odp_grid_create", "odp_grid_destroy", "odp_grid_info", "odp_hj_solve", "odp_hj_solve_host",
            "odp_partition_extent", "odp_comm_unique_id", "odp_grid_partition", "odp_grid_local_extent",
            "odp_last_launch_count", "odp_last_error", "odp_version", "odp_ttr_solve", "odp_ttr_solve_host",
-           "odp_vi_solve", "odp_vi_solve_host")
+           "odp_vi_solve", "odp_vi_solve_host", "odp_loopback_create", "odp_grid_partition_loopback",
+           "odp_loopback_destroy")
 MDP_MODELS = {"HOLONOMIC": 0, "DUBINS3D": 1}
 
 
@@ -105,6 +106,12 @@ def _load():
     lib.odp_comm_unique_id.restype = ctypes.c_int
     lib.odp_grid_partition.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int]
     lib.odp_grid_partition.restype = ctypes.c_int
+    lib.odp_loopback_create.argtypes = [ctypes.c_int, ctypes.POINTER(vp)]
+    lib.odp_loopback_create.restype = ctypes.c_int
+    lib.odp_grid_partition_loopback.argtypes = [vp, ctypes.c_int, vp]
+    lib.odp_grid_partition_loopback.restype = ctypes.c_int
+    lib.odp_loopback_destroy.argtypes = [vp]
+    lib.odp_loopback_destroy.restype = None
     lib.odp_grid_local_extent.argtypes = [vp, I64, I64]
     lib.odp_grid_local_extent.restype = ctypes.c_int
     lib.odp_last_launch_count.argtypes = [vp]
@@ -191,6 +198,12 @@ class Grid:
         b, c = self.local_extent()
         self.local_N = (c,) + self.N[1:]
 
+    def partition_loopback(self, rank: int, lb: "Loopback"):
+        """odp_grid_partition_loopback: rank `rank`'s slab on a one-GPU loopback transport (tests)."""
+        _check(_lib.odp_grid_partition_loopback(self.handle, int(rank), lb.handle))
+        b, c = self.local_extent()
+        self.local_N = (c,) + self.N[1:]
+
     def local_extent(self):
         b, c = ctypes.c_int64(), ctypes.c_int64()
         _check(_lib.odp_grid_local_extent(self.handle, ctypes.byref(b), ctypes.byref(c)))
@@ -209,6 +222,21 @@ class Grid:
             self.close()
         except Exception:
             pass
+
+
+class Loopback:
+    """odp_loopback_create / odp_loopback_destroy: the one-GPU test transport of nranks slab handles."""
+
+    def __init__(self, nranks: int):
+        h = ctypes.c_void_p()
+        _check(_lib.odp_loopback_create(int(nranks), ctypes.byref(h)))
+        self.handle = h
+        self.nranks = int(nranks)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.odp_loopback_destroy(self.handle)
+            self.handle = None
 
 
 class SolveInfo(dict):

@@ -512,7 +512,6 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     uint32_t *t_snb = reinterpret_cast<uint32_t *>(t_soff + 32);           // [32] bytes (0 = skip)
     int *t_ring = reinterpret_cast<int *>(t_snb + 32);                      // [8]
     int *uq = t_ring + 8;                                                   // [NST] unit queue (producer -> compute warps)
-    int *prec = uq + 4;                                                     // [3 NST + 1] issued steps: unit, index, first; end marker
     auto make_table = [&](const MarchUnit &U) {
         const int lane = tid & 31;
         int oid[NSA], oN[NSA];

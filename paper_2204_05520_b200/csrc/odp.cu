@@ -14,7 +14,11 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
+#include <condition_variable>
 #include <functional>
+#include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -69,6 +73,8 @@ struct Api {
     result_t (*GroupStart)() = nullptr;
     result_t (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(result_t) = nullptr;
+    result_t (*CommGetAsyncError)(comm_t, result_t *) = nullptr;   // failure detection (optional)
+    result_t (*CommAbort)(comm_t) = nullptr;
 };
 static Api &api() {
     static Api a;
@@ -87,6 +93,8 @@ static Api &api() {
     a.GroupStart = (result_t(*)())dlsym(h, "ncclGroupStart");
     a.GroupEnd = (result_t(*)())dlsym(h, "ncclGroupEnd");
     a.GetErrorString = (const char *(*)(result_t))dlsym(h, "ncclGetErrorString");
+    a.CommGetAsyncError = (result_t(*)(comm_t, result_t *))dlsym(h, "ncclCommGetAsyncError");
+    a.CommAbort = (result_t(*)(comm_t))dlsym(h, "ncclCommAbort");
     a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.AllReduce && a.GroupStart &&
            a.GroupEnd && a.GetErrorString;
     return a;
@@ -463,6 +471,8 @@ static KernelSet select_set(int dyn, int n, int R) { return R == 1 ? select_set_
 // ------------------------------------------------------------------------------------------------
 // grid handle
 // ------------------------------------------------------------------------------------------------
+struct odp_loopback;
+extern "C" void odp_loopback_destroy(odp_loopback *lb);
 struct odp_grid {
     int n = 0;
     int64_t N[MAXD] = {0};
@@ -473,6 +483,7 @@ struct odp_grid {
     int rank = 0, nranks = 1;
     int64_t i0b = 0, n0 = 0;      // first owned axis-0 plane, owned planes
     nccl::comm_t comm = nullptr;
+    odp_loopback *lb = nullptr;   // test transport: slabs of one process on one GPU (odp_grid_partition_loopback)
     float *d_range = nullptr;     // [-minD, maxD, maxabs, nan] of the current stage (allreduced)
     float *d_amax = nullptr;      // per-CTA alpha^max of k_amax3 (DEPS3 functors)
     // device cache (allocated lazily on the device current at the first solve)
@@ -607,6 +618,7 @@ extern "C" odp_status odp_grid_partition(odp_grid *g, int rank, int nranks, cons
     free_device(g);                       // working buffers are sized by the slab
     if (g->comm && nccl::api().ok) nccl::api().CommDestroy(g->comm);
     g->comm = nullptr;
+    g->lb = nullptr;
     g->rank = rank; g->nranks = nranks; g->i0b = b; g->n0 = c;
     if (id128) {            // (nranks = 1 with an id: a 1-rank communicator -- the multi-GPU code path)
         nccl::Api &a = nccl::api();
@@ -748,11 +760,142 @@ static GridDev make_griddev(const odp_grid *g) {
     return d;
 }
 
+// ------------------------------------------------------------------------------------------------
+// Loopback transport (tests: the multi-rank slab path on ONE GPU).  The P slab handles of one
+// process, each driven by its own host thread, exchange halo planes by device-to-device copies and
+// reduce their range records with a max kernel.  Ordering uses only stream events plus a host
+// barrier per collective (every rank enqueues the same collectives in the same order, as with
+// NCCL: same dt sequence, same launch chunks); nothing on the device waits on another rank's
+// kernel, so ranks may run concurrently or one after the other.
+// ------------------------------------------------------------------------------------------------
+struct odp_loopback {
+    int n = 0;
+    std::mutex m;
+    std::condition_variable cv;
+    long long gen = 0;
+    int count = 0;
+    std::vector<odp_grid *> g;            // by rank
+    std::vector<float *> w;               // each rank's stage input of the current exchange
+    std::vector<cudaEvent_t> ready, done; // per rank: my data is final / I finished reading the others'
+    float *rec = nullptr;                 // [n][2 MAXD + 2] range records (device, on the ranks' GPU)
+    void barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        const long long g0 = gen;
+        if (++count == n) { count = 0; ++gen; cv.notify_all(); }
+        else cv.wait(lk, [&] { return gen != g0; });
+    }
+};
+
+__global__ void k_rec_max(const float *rec, int nr, int cnt, float *out) {
+    const int q = threadIdx.x;
+    if (q >= cnt) return;
+    float r = rec[q];
+    for (int k = 1; k < nr; ++k) r = fmaxf(r, rec[k * (2 * MAXD + 2) + q]);
+    out[q] = r;
+}
+
+extern "C" odp_status odp_loopback_create(int nranks, odp_loopback **out) {
+    g_err.clear();
+    if (!out || nranks < 1 || nranks > 64) return fail(ODP_EINVAL, "loopback of %d ranks", nranks);
+    odp_loopback *lb = new (std::nothrow) odp_loopback();
+    if (!lb) return fail(ODP_ENOMEM, "host allocation");
+    lb->n = nranks;
+    lb->g.assign(nranks, nullptr);
+    lb->w.assign(nranks, nullptr);
+    lb->ready.assign(nranks, nullptr);
+    lb->done.assign(nranks, nullptr);
+    for (int r = 0; r < nranks; ++r) {
+        if (cudaEventCreateWithFlags(&lb->ready[r], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&lb->done[r], cudaEventDisableTiming) != cudaSuccess) {
+            odp_loopback_destroy(lb);
+            return fail(ODP_ECUDA, "loopback events");
+        }
+    }
+    if (cudaMalloc(&lb->rec, (size_t)nranks * (2 * MAXD + 2) * sizeof(float)) != cudaSuccess) {
+        odp_loopback_destroy(lb);
+        return fail(ODP_ECUDA, "loopback records");
+    }
+    *out = lb;
+    return ODP_OK;
+}
+
+extern "C" void odp_loopback_destroy(odp_loopback *lb) {
+    if (!lb) return;
+    for (auto e : lb->ready) if (e) cudaEventDestroy(e);
+    for (auto e : lb->done) if (e) cudaEventDestroy(e);
+    cudaFree(lb->rec);
+    delete lb;
+}
+
+extern "C" odp_status odp_grid_partition_loopback(odp_grid *g, int rank, odp_loopback *lb) {
+    g_err.clear();
+    if (!g || !lb) return fail(ODP_EINVAL, "NULL grid / loopback");
+    const int nranks = lb->n;
+    if (rank < 0 || rank >= nranks) return fail(ODP_EINVAL, "rank %d of %d", rank, nranks);
+    if (nranks > 1 && g->per[0]) return fail(ODP_EINVAL, "axis 0 is periodic: slab partition not supported");
+    if (nranks > 1 && g->N[0] < (int64_t)R_MAX * nranks)
+        return fail(ODP_EINVAL, "N[0]=%lld < %d planes per rank", (long long)g->N[0], R_MAX);
+    int64_t b = 0, c = 0;
+    odp_status st = odp_partition_extent(g->N[0], nranks, rank, &b, &c);
+    if (st) return st;
+    free_device(g);
+    if (g->comm && nccl::api().ok) nccl::api().CommDestroy(g->comm);
+    g->comm = nullptr;
+    g->rank = rank; g->nranks = nranks; g->i0b = b; g->n0 = c;
+    g->lb = lb;
+    lb->g[rank] = g;
+    return ODP_OK;
+}
+
+static odp_status lb_halo_exchange(odp_grid *g, float *W, int R, cudaStream_t s) {
+    odp_loopback *lb = g->lb;
+    const int me = g->rank;
+    const size_t plane = (size_t)plane_of(g), cnt = (size_t)R * plane;
+    lb->w[me] = W;
+    CUDA_TRY(cudaEventRecord(lb->ready[me], s));
+    lb->barrier();                                           // every rank's W recorded
+    if (me > 0) {                                            // rank-1's last R planes -> my low halo
+        const odp_grid *o = lb->g[me - 1];
+        CUDA_TRY(cudaStreamWaitEvent(s, lb->ready[me - 1], 0));
+        CUDA_TRY(cudaMemcpyAsync(W - cnt, lb->w[me - 1] + (size_t)(o->n0 - R) * plane, cnt * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, s));
+    }
+    if (me < lb->n - 1) {                                    // rank+1's first R planes -> my high halo
+        CUDA_TRY(cudaStreamWaitEvent(s, lb->ready[me + 1], 0));
+        CUDA_TRY(cudaMemcpyAsync(W + (size_t)g->n0 * plane, lb->w[me + 1], cnt * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, s));
+    }
+    CUDA_TRY(cudaEventRecord(lb->done[me], s));
+    lb->barrier();                                           // every rank's reads enqueued
+    if (me > 0) CUDA_TRY(cudaStreamWaitEvent(s, lb->done[me - 1], 0));   // my planes read before I overwrite them
+    if (me < lb->n - 1) CUDA_TRY(cudaStreamWaitEvent(s, lb->done[me + 1], 0));
+    return ODP_OK;
+}
+
+static odp_status lb_range_allreduce(odp_grid *g, int n, cudaStream_t s) {
+    odp_loopback *lb = g->lb;
+    const int me = g->rank, cnt = 2 * n + 2;
+    CUDA_TRY(cudaMemcpyAsync(lb->rec + (size_t)me * (2 * MAXD + 2), g->d_range, cnt * sizeof(float),
+                             cudaMemcpyDeviceToDevice, s));
+    CUDA_TRY(cudaEventRecord(lb->ready[me], s));
+    lb->barrier();
+    for (int r = 0; r < lb->n; ++r)
+        if (r != me) CUDA_TRY(cudaStreamWaitEvent(s, lb->ready[r], 0));
+    k_rec_max<<<1, 32, 0, s>>>(lb->rec, lb->n, cnt, g->d_range);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(lb->done[me], s));
+    lb->barrier();
+    for (int r = 0; r < lb->n; ++r)                          // every rank read my record before I rewrite it
+        if (r != me) CUDA_TRY(cudaStreamWaitEvent(s, lb->done[r], 0));
+    return ODP_OK;
+}
+
 // Halo planes of a stage input W (local plane 0) from the axis-0 neighbours (north_star: NCCL
 // send/recv per RK stage): my first R planes go to rank-1's high halo, my last R planes to rank+1's
 // low halo.  Slabs are contiguous row-major ranges, so every message is one contiguous range.
 static odp_status halo_exchange(odp_grid *g, float *W, int R, cudaStream_t s) {
     if (g->nranks <= 1) return ODP_OK;
+    if (g->lb) return lb_halo_exchange(g, W, R, s);
     nccl::Api &a = nccl::api();
     const size_t plane = (size_t)plane_of(g), cnt = (size_t)R * plane;
     NCCL_TRY(a.GroupStart());
@@ -770,9 +913,44 @@ static odp_status halo_exchange(odp_grid *g, float *W, int R, cudaStream_t s) {
 
 // allreduce(max) of the stage's range record [-minD, maxD, maxabs, nan] over the ranks
 static odp_status range_allreduce(odp_grid *g, int n, cudaStream_t s) {
+    if (g->lb) return lb_range_allreduce(g, n, s);
     if (!g->comm) return ODP_OK;
     NCCL_TRY(nccl::api().AllReduce(g->d_range, g->d_range, (size_t)(2 * n + 2), nccl::Float32, nccl::Max, g->comm, s));
     return ODP_OK;
+}
+
+// Host wait for a stream of a partitioned solve.  With an NCCL communicator the wait polls (no
+// blocking synchronize): a peer that failed or vanished leaves our NCCL kernels waiting forever, so
+// ncclCommGetAsyncError is checked every millisecond and the communicator is aborted on an error or
+// after ODP_NCCL_TIMEOUT_S seconds (default 600) without progress -- the solve then returns
+// ODP_ENCCL instead of hanging.
+static odp_status sync_stream(odp_grid *g, cudaStream_t s) {
+    if (!g->comm) {
+        CUDA_TRY(cudaStreamSynchronize(s));
+        return ODP_OK;
+    }
+    nccl::Api &a = nccl::api();
+    double limit = 600.0;
+    if (const char *e = getenv("ODP_NCCL_TIMEOUT_S")) limit = atof(e);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        const cudaError_t q = cudaStreamQuery(s);
+        if (q == cudaSuccess) return ODP_OK;
+        if (q != cudaErrorNotReady) return fail(ODP_ECUDA, "stream: %s", cudaGetErrorString(q));
+        nccl::result_t ae = 0;
+        if (a.CommGetAsyncError && a.CommGetAsyncError(g->comm, &ae) == 0 && ae != 0) {
+            if (a.CommAbort) a.CommAbort(g->comm);
+            g->comm = nullptr;
+            return fail(ODP_ENCCL, "NCCL asynchronous error: %s (communicator aborted)", a.GetErrorString(ae));
+        }
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (el > limit) {
+            if (a.CommAbort) a.CommAbort(g->comm);
+            g->comm = nullptr;
+            return fail(ODP_ENCCL, "no progress for %.0f s (peer failure?): communicator aborted", el);
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
 }
 
 static const int kWantParams[7] = {2, 3, 3, 5, 3, 3, 5};
@@ -940,7 +1118,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
     };
     odp_status cst = ODP_OK;     // first communication failure (NCCL calls are enqueued, not checked per launch)
     auto launch_guard = [&](int last_stage) {
-        if (g->comm) {
+        if (g->comm || g->lb) {
             ks.red<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, g->d_range);
             if (cst == ODP_OK) cst = range_allreduce(g, n, s);
             ks.guard<<<1, 256, 0, s>>>(g->d_partials, nparts, g->d_state, g->d_range, last_stage);
@@ -954,7 +1132,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
     const int namax = ks.amax3 ? nsm : 0;           // k_amax3 CTAs (DEPS3 functors)
     auto launch_fin = [&](int stage_in_step, int final_check) {
         const float *rng = nullptr;
-        if (g->comm) {
+        if (g->comm || g->lb) {
             ks.red<<<1, 256, 0, s>>>(g->d_partials, nparts1, g->d_state, g->d_range);
             if (cst == ODP_OK) cst = range_allreduce(g, n, s);
             rng = g->d_range;
@@ -1047,7 +1225,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
     // timing (per-launch events) or an NCCL communicator.
     constexpr int GS = 8;
     const int ug = opts ? opts->use_graph : 0;
-    const bool graphs = !timed && !g->comm && (ug == 1 || (ug == 0 && local_points(g) <= (1LL << 25)));
+    const bool graphs = !timed && !g->comm && !g->lb && (ug == 1 || (ug == 0 && local_points(g) <= (1LL << 25)));
     cudaGraphExec_t gexec[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
     long long glaunch[2] = {0, 0};          // kernel launches per replay, by step kind
     auto graph_of = [&](int kind_sp, int a0, cudaGraphExec_t *out_exec) -> odp_status {
@@ -1078,7 +1256,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
         k_begin<<<1, 1, 0, s>>>(g->d_state, tau[k]);
         ++g->launches;
         CUDA_TRY(cudaMemcpyAsync(g->h_state, g->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
+        if (odp_status ss = sync_stream(g, s)) return ss;
         long long s0 = g->h_state->steps;
         int chunk = 2;
         std::vector<int> step_of_launch;
@@ -1104,7 +1282,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
             CUDA_TRY(cudaGetLastError());
             if (cst) return cst;
             CUDA_TRY(cudaMemcpyAsync(g->h_state, g->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-            CUDA_TRY(cudaStreamSynchronize(s));
+            if (odp_status ss = sync_stream(g, s)) return ss;
             const long long done = g->h_state->steps - s0;
             s0 = g->h_state->steps;
             if (accuracy == ODP_LOW && (done & 1)) cur ^= 1;
@@ -1143,7 +1321,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
         g->launches += 3;
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaMemcpyAsync(g->h_state, g->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
+        if (odp_status ss = sync_stream(g, s)) return ss;
         if (g->h_state->status) rs = ODP_ENUMERIC;
     }
     if (opts) {

@@ -87,33 +87,7 @@ def assert_parity_one_step(gpu, ref, R, tol=TOL, band=BAND, what=""):
     return out_err, in_err, int(amb.sum())
 
 
-def assert_parity_multistep_medium(gpu, ref, tol=TOL, what="", q=0.999, max_tol=2e-3):
-    """Parity over MANY steps of MEDIUM (ENO2 + RK2).
-
-    ENO2 picks its stencil by comparing |second differences|; that choice is a discontinuous
-    function of the data, so two float evaluations of the same scheme (float32 GPU, float64
-    oracle -- or the oracle against itself with a 1-ulp perturbed input) occasionally pick
-    differently at a near-tie and then differ at that node by a few 1e-4 (reading A28; the paper's
-    own Table 1 shows second-order implementations disagreeing by up to 0.25).  Bar:
-      * the q-quantile (99.9 %) of |V_gpu - V_oracle| <= 1e-4 (the north_star tolerance),
-      * max |V_gpu - V_oracle| <= 2e-3 (isolated tie events only),
-      * membership identical wherever |V_oracle| >= 1e-3, and outside |V_oracle| < 1e-4 on all
-        but 1e-5 of the nodes.
-    """
-    g = np.asarray(gpu, dtype=np.float64)
-    r = np.asarray(ref.out if hasattr(ref, "out") else ref, dtype=np.float64)
-    d = np.abs(g - r)
-    qv = float(np.quantile(d, q))
-    mx = float(d.max())
-    memb = (g <= 0) != (r <= 0)
-    hard = int((memb & (np.abs(r) >= 1e-3)).sum())
-    soft = float((memb & (np.abs(r) >= BAND)).mean())
-    assert qv <= tol and mx <= max_tol and hard == 0 and soft <= 1e-5, \
-        f"{what}: q{q} {qv:.3e}, max {mx:.3e}, membership mismatches |V|>=1e-3: {hard}, band fraction {soft:.2e}"
-    return qv, mx
-
-
-def oracle_envelope(w, V0, nperturb=2, **kw):
+def oracle_envelope(w, V0, nperturb=6, **kw):
     """The oracle's own sensitivity to float32-level perturbations (reading A28).
 
     ENO2 (MEDIUM) selects its stencil by comparing |second differences|; that choice is a
@@ -136,20 +110,91 @@ def oracle_envelope(w, V0, nperturb=2, **kw):
 
 
 def assert_parity_envelope(gpu, base, E, tol=TOL, band=BAND, what=""):
-    """Strict 1e-4 parity where the oracle itself is stable, the oracle's own spread elsewhere.
-
-      (1) max |V_gpu - V_oracle| <= max(tol, 2 max E)
-      (2) nodes with |dV| > tol are no more frequent than 2x the nodes with E > tol (+0.1 % slack)
-      (3) membership identical wherever |V_oracle| >= max(band, E)
-    """
+    """MEDIUM (ENO2 + TVD-RK2) over many steps: the GPU result must be indistinguishable from another
+    float32 realisation of the scheme, judged against the oracle's own float32 envelope E
+    (oracle_envelope: float32 storage and 1-ulp input perturbations, computed by the oracle alone).
+    ENO2 selects its stencil by comparing |second differences|, a discontinuous function of the data:
+    float32 realisations flip isolated near-tie picks at DIFFERENT nodes, so a node-by-node bar on
+    "oracle-stable" nodes does not hold even between two oracle realisations (reading A28; the
+    measurements are in DESIGN.md §5).  The bar:
+      (1) max |V_gpu - V_oracle| <= max(tol, 2 max E);
+      (2) nodes off by more than tol: no more than 2 x the nodes with E > tol (+ 4);
+      (3) the 99.9 % quantile of |V_gpu - V_oracle| <= max(tol / 10, 2 x that of E) (bulk agreement);
+      (4) membership (V <= 0) identical wherever |V_oracle| >= max(band, E)."""
     g = np.asarray(gpu, dtype=np.float64)
     r = base.out
     d = np.abs(g - r)
     emax = float(E.max())
     assert d.max() <= max(tol, 2 * emax), f"{what}: max|dV| {d.max():.3e} > max(tol, 2 max E = {2 * emax:.3e})"
-    frac_g = float((d > tol).mean())
-    frac_e = float((E > tol).mean())
-    assert frac_g <= 2 * frac_e + 1e-3, f"{what}: {frac_g:.4%} of nodes off by > tol vs oracle spread {frac_e:.4%}"
+    ng, ne = int((d > tol).sum()), int((E > tol).sum())
+    assert ng <= 2 * ne + 4, f"{what}: {ng} nodes off by > tol vs the oracle's own spread {ne}"
+    qd, qe = float(np.quantile(d, 0.999)), float(np.quantile(E, 0.999))
+    assert qd <= max(tol / 10, 2 * qe), f"{what}: q99.9 |dV| {qd:.3e} vs the oracle's {qe:.3e}"
     memb = ((g <= 0) != (r <= 0)) & (np.abs(r) >= np.maximum(band, E))
     assert memb.sum() == 0, f"{what}: {int(memb.sum())} membership mismatches outside the band"
-    return float(d.max()), emax, frac_g, frac_e
+    return float(d.max()), emax, ng, ne
+
+
+# ------------------------------------------------------------------------------------------------
+# Windowed oracle (pin Z12, SURVEY.md §8(c)): after s stages a node depends only on the nodes within
+# R s of it along each axis (Alg. 2 is a star stencil of radius R per stage; the BRT min is
+# pointwise), provided alpha^max -- hence dt -- is the full grid's.  For dynamics whose alpha does
+# not depend on the derivative range (RANGE_FREE, e.g. DOUBLEINT6D) the full grid's alpha^max is a
+# function of the coordinate extremes only, so a float64 oracle solve on a sub-box (clipped at the
+# real faces, where the ghost rule is the real one) reproduces the full solve at the box centre.
+# ------------------------------------------------------------------------------------------------
+def full_grid_amax(w):
+    """alpha^max of the full grid (Alg. 2 l.164) from the oracle's own alpha at every combination
+    of the axes' extreme nodes (alpha of the compiled-in RANGE_FREE dynamics is monotone in |x|)."""
+    import itertools
+    import oracle
+    from inputs import axis_nodes
+    ax = [axis_nodes(n, l, h, bool(p)) for n, l, h, p in zip(w.N, w.lo, w.hi, w.periodic)]
+    cand = [sorted(set([a[0], a[-1], a[len(a) // 2]])) for a in ax]
+    n = len(w.N)
+    amax = np.zeros(n)
+    for x in itertools.product(*cand):
+        amax = np.maximum(amax, oracle.alpha(w.dynamics, w.params, np.array(x), -np.ones(n), np.ones(n)))
+    return amax
+
+
+def windowed_oracle(w, nodes, stages_per_step, steps, amax):
+    """Values of the float64 oracle solve of `w` (one output time, tau = w.tau[-1]) at `nodes`
+    (list of index tuples), each from a sub-box of half-width R * stages around the node."""
+    import oracle
+    from inputs import axis_nodes, make_v0
+    R = 1 if w.accuracy == "low" else 2
+    hw = R * stages_per_step * steps
+    ax = [axis_nodes(n, l, h, bool(p)) for n, l, h, p in zip(w.N, w.lo, w.hi, w.periodic)]
+    vals = []
+    for node in nodes:
+        box = []
+        for d, i in enumerate(node):
+            if w.periodic[d]:
+                box.append((0, w.N[d]))
+            else:
+                b = max(0, i - hw)
+                e = min(w.N[d], i + hw + 1)
+                box.append((b, e - b))
+        V0 = make_v0(w, box=box)
+        lo = tuple(float(ax[d][b]) for d, (b, c) in enumerate(box))
+        hi = tuple(float(ax[d][b + c - 1]) if not w.periodic[d] else w.hi[d] for d, (b, c) in enumerate(box))
+        N = tuple(c for _, c in box)
+        r = oracle.hj_solve(N, lo, hi, w.periodic_mask, w.dynamics, w.params, V0, w.tau, w.accuracy, w.mode,
+                            cfl=w.cfl, amax_fixed=amax)
+        local = tuple(i - b for i, (b, _) in zip(node, box))
+        vals.append((float(r.out[-1][local]), r.steps, r.stages))
+    return vals
+
+
+def sample_nodes(N, count, seed, faces=True):
+    """Seeded node sample: uniform nodes plus (faces=True) nodes on every face band of every axis."""
+    rng = np.random.default_rng(seed)
+    out = [tuple(int(rng.integers(0, n)) for n in N) for _ in range(count)]
+    if faces:
+        for d, n in enumerate(N):
+            for fv in (0, 1, n - 2, n - 1):
+                x = [int(rng.integers(0, m)) for m in N]
+                x[d] = fv
+                out.append(tuple(x))
+    return out

@@ -100,3 +100,26 @@ def test_split_pass1_overlap_path_is_bitwise(name, N, acc, comm, monkeypatch):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(out2.cpu().numpy(), ref.cpu().numpy())
     assert info2["kernel_ms"]["pass1"] > 0
+
+
+@pytest.mark.parametrize("name,N,acc", [("c4", (12, 10, 12, 10, 12, 10), "medium"), ("c4", (12, 10, 12, 10, 12, 10), "low"),
+                                        ("c1", (41, 41, 36), "low"), ("c3", (12, 11, 12, 10, 8), "medium")])
+def test_single_pass_matches_the_oracle(name, N, acc):
+    # SURVEY.md §8(f1) against the float64 oracle directly (not only against the two-pass GPU solve):
+    # LOW strict 1e-4, MEDIUM the oracle-envelope bar (reading A28)
+    import torch
+    import paper_2204_05520_b200 as odp
+    from tests.parity_util import assert_parity, assert_parity_envelope, oracle_envelope, run_oracle
+    w = coarsened(CONFIGS[name], N, tau=(0.0, 0.2, 0.5))
+    w = w.__class__(**{**w.__dict__, "accuracy": acc, "cfl": 0.8 if acc == "low" else 0.5})
+    V0 = make_v0(w, seed=3)
+    out, info = odp.solve_workload(w, torch.from_numpy(V0).cuda(), single_pass=True)
+    assert info["single_pass"]
+    out = out.cpu().numpy()
+    if acc == "low":
+        ref = run_oracle(w, V0)
+        assert_parity(out, ref.out, what=f"single pass {name}")
+    else:
+        ref, E = oracle_envelope(w, V0)
+        assert_parity_envelope(out, ref, E, what=f"single pass {name}")
+    assert info["steps"] == ref.steps

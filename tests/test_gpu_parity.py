@@ -7,8 +7,8 @@ import numpy as np
 import pytest
 
 from inputs import CONFIGS, Workload, coarsened, holonomic, make_v0
-from tests.parity_util import (TOL, assert_parity, assert_parity_multistep_medium, assert_parity_one_step, covers,
-                                run_gpu, run_oracle)
+from tests.parity_util import (TOL, assert_parity, assert_parity_envelope, assert_parity_one_step, covers,
+                                oracle_envelope, run_gpu, run_oracle)
 
 pytestmark = pytest.mark.gpu
 
@@ -43,12 +43,13 @@ def test_parity_small(case, acc, mode, kernel):
     for seed in (None, 0):
         V0 = make_v0(w, seed=seed)
         out, info = run_gpu(w, V0, kernel=kernel)
-        ref = run_oracle(w, V0)
         what = f"{dyn} {acc} {mode} {kernel} seed={seed}"
         if acc == "low":
+            ref = run_oracle(w, V0)
             assert_parity(out, ref.out, what=what)
-        else:   # ENO2 decisions are discontinuous: quantile bar over many steps (A28)
-            assert_parity_multistep_medium(out, ref, q=0.99, what=what)
+        else:   # ENO2 picks flip at float32 near-ties: strict where the oracle is stable (A28)
+            ref, E = oracle_envelope(w, V0)
+            assert_parity_envelope(out, ref, E, what=what)
         assert info["steps"] == ref.steps and info["stages"] == ref.stages
         assert abs(info["tau_reached"] - ref.tau_reached) < 1e-12
 
