@@ -34,29 +34,23 @@ UNIT = "point-stages/s"
 
 # algorithmic HBM bytes per point of one launch (SURVEY.md §8(a) table "Bytes per point per stage")
 PASS1_BYTES = 4                                     # read W
-PASS2_BYTES = {("low", "brt"): 12, ("low", "brs"): 8,          # Euler: R W, (R V0), W V'
-               ("medium", "brt"): 12, ("medium", "brs"): 10}   # mean of RK stage 1 (8) and stage 2 (16 / 12)
+PASS2_BYTES = {("low", "brt"): 12, ("low", "brs"): 8,                      # Euler: R W, (R V0), W V'
+               ("medium", "brt", 1): 8, ("medium", "brs", 1): 8,            # RK stage 1: R Vn, W V1
+               ("medium", "brt", 2): 16, ("medium", "brs", 2): 12}          # RK stage 2: R V1, R Vn, (R V0), W Vn
 STAGE_BYTES = {("low", "brt"): 16, ("low", "brs"): 12, ("medium", "brt"): 16, ("medium", "brs"): 14}
+N_SMSP = 148 * 4                                    # issue slots per cycle of the chip (warp instructions)
 
 
-# The march kernels read every W tile through L2 several times: per node and pass,
-# 2R+1 ... tiles of the side axes.  L2-to-SM bytes per point: pass 1 = (1 centre + (2R-1 interior
-# edge-assigned side tiles) x side axes) x 4 B; pass 2 = (1 + 2R x side axes) x 4 B of W plus the
-# Vn / target / output streams (mean of the RK stages).  Cap: the LTS throughput of
-# /opt/skills/guides/B300_MICROARCH.md (~6300 B/cycle full chip) at the measured SM clock.
-def l2_path(w, pass1_ms, pass2_ms, Pl, sm_mhz=1900.0):
-    n = len(w.N)
-    R = 1 if w.accuracy == "low" else 2
-    side = max(0, n - 3)
-    p1 = (1 + (2 * R - (1 if R == 2 else 0)) * side) * 4
-    extra = {("low", "brt"): 8, ("low", "brs"): 4, ("medium", "brt"): 10, ("medium", "brs"): 8}[(w.accuracy, w.mode)]
-    p2 = (1 + 2 * R * side) * 4 + extra
-    cap = 6300.0 * sm_mhz * 1e6 / 1e12
-    a1 = p1 * Pl / (pass1_ms / 1e3) / 1e12
-    a2 = p2 * Pl / (pass2_ms / 1e3) / 1e12
-    return {"unit": "TB/s", "cap": cap, "pass1_bytes_per_point": p1, "pass1_achieved": a1, "pass1_frac": a1 / cap,
-            "pass2_bytes_per_point": p2, "pass2_achieved": a2, "pass2_frac": a2 / cap,
-            "note": "L2-to-SM tile traffic of the march kernels vs the LTS throughput cap (context for the HBM frac)"}
+def ncu_kernel_profile(name):
+    """Per-launch figures of one `ncu --set full` capture of the workload's kernels (committed under
+    profiles/, written by tools/make_profiles.py): DRAM bytes, warp instructions, issue-active."""
+    prof = os.path.join(ROOT, "profiles", "ncu_kernels.json")
+    if not os.path.exists(prof):
+        return {}
+    try:
+        return json.load(open(prof)).get(name, {})
+    except Exception:
+        return {}
 
 
 def measured_peaks():
@@ -163,8 +157,10 @@ def oracle_sample(w, target_s: float = 15.0):
     side = max(6, min(side, max(w.N)))
     sub = box(side)
     el, work, stages = timed(sub)
+    full_s = w.points * (stages * 1.0) / (work / el)
     sample = (f"oracle float64 on a {'x'.join(map(str, sub.N))} centred sub-box of {w.name} (same spacing, "
-              f"dynamics, target), one time step = {stages} RK stages, {el:.1f} s")
+              f"dynamics, target), one time step = {stages} RK stages, {el:.1f} s; the rate is per point-stage "
+              f"(one time step of the full {w.name} grid would take ~{full_s:.0f} s at it)")
     return work / el, sample, cores, el, work
 
 
@@ -296,7 +292,13 @@ def run_ttr(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, sample, cores, el, work = ttr_oracle_sample(w, target_s=args.ref_seconds)
-        line["cpu_baseline"] = {"value": rate, "unit": TTR_UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        line["cpu_baseline"] = {"value": rate, "unit": TTR_UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                                "ordering": ("different iteration orders: the oracle runs Alg. 3 as printed (in-place "
+                                             "Gauss-Seidel, 8 alternating orderings, §4.3), the GPU Jacobi (reading "
+                                             "A35, %d iterations at %s); Gauss-Seidel reaches the same fixed point in "
+                                             "fewer sweeps, so the node-iterations/s ratio compares iteration "
+                                             "throughput and overstates the time-to-solution ratio" %
+                                             (iters // max(1, args.steps), "x".join(map(str, w.N))))}
     if rank == 0:
         print(json.dumps(line), flush=True)
     g.close()
@@ -586,7 +588,7 @@ def run_ours(args):
         info = one()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kms = {"pass1": 0.0, "pass2": 0.0, "control": 0.0}
+    kms = {"pass1": 0.0, "pass2": 0.0, "control": 0.0, "pass2_rk2": 0.0}
     launches = 0
     with ClockSampler(local) as clk:
         barrier()
@@ -625,19 +627,34 @@ def run_ours(args):
 
     peak, peak_kind = measured_peaks()
     key = (w.accuracy, w.mode)
-    Pl = g.points                                  # this rank's points (the kernel's launch unit)
-    n_pass2 = stages                               # one pass-2 launch per stage (one timed solve)
-    pass2_ms = kms["pass2"] / n_pass2
-    pass1_ms = kms["pass1"] / n_pass2
-    achieved = PASS2_BYTES[key] * Pl / (pass2_ms / 1e3) / 1e9
-    stage_gbs = STAGE_BYTES[key] * Pl / ((pass1_ms + pass2_ms) / 1e3) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof) and world == 1:
-        try:
-            traffic = json.load(open(prof)).get(f"{w.name}:pass2")     # DRAM bytes per launch (ncu --set full)
-        except Exception:
-            traffic = None
+    Pl = g.points                                  # this rank's points (the kernels' launch unit)
+    steps_t = tinfo["steps"]
+    pass1_ms = kms["pass1"] / stages               # one pass-1 launch per stage (the timed solve)
+    sm_hz = (clocks.get("sm_mhz") or 1900.0) * 1e6
+    prof = ncu_kernel_profile(w.name) if world == 1 else {}
+    if w.accuracy == "medium":
+        p2 = {"pass2_rk1": ((kms["pass2"] - kms["pass2_rk2"]) / steps_t, PASS2_BYTES[key + (1,)]),
+              "pass2_rk2": (kms["pass2_rk2"] / steps_t, PASS2_BYTES[key + (2,)])}
+    else:
+        p2 = {"pass2": (kms["pass2"] / stages, PASS2_BYTES[key])}
+    kernels = {"pass1": (pass1_ms, PASS1_BYTES)}
+    kernels.update(p2)
+    ktab = {}
+    for kname, (ms, bpp) in kernels.items():
+        ach = bpp * Pl / (ms / 1e3) / 1e9
+        ent = {"avg_launch_ms": ms, "bytes_per_point": bpp, "achieved": ach, "frac": ach / peak}
+        pk = prof.get(kname)
+        if pk:
+            # issue roofline: the launch's warp instructions at one per SMSP per cycle, at the live clock
+            t_issue = pk["warp_inst"] / (N_SMSP * sm_hz) * 1e3
+            ent.update({"traffic": pk["dram_bytes"], "traffic_per_point": pk["dram_bytes"] / Pl,
+                        "warp_inst": pk["warp_inst"], "issue_bound_ms": t_issue, "issue_frac": t_issue / ms,
+                        "ncu_issue_active": pk["issue_active_pct"] / 100.0})
+        ktab[kname] = ent
+    dom = max(p2, key=lambda k: p2[k][0])          # the dominant (longest) pass-2 launch
+    d = ktab[dom]
+    stage_ms = pass1_ms + sum(v[0] for v in p2.values()) / len(p2)
+    stage_gbs = STAGE_BYTES[key] * Pl / (stage_ms / 1e3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
@@ -649,18 +666,25 @@ def run_ours(args):
                    if Pl * 4 > 126e6 else "fits L2",
                    "parallelism": "single GPU" if world == 1 else f"axis-0 slabs x{world} (NCCL halo + allreduce)",
                    "slab": [i0b, n0]},
-        "roofline": {"bound": "hbm", "kernel": "pass2 (D+-, H, dissipation, RK stage, BRT min)",
-                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_kind": peak_kind,
-                     "bytes_per_point": PASS2_BYTES[key], "avg_launch_ms": pass2_ms,
-                     "stage": {"bytes_per_point": STAGE_BYTES[key], "achieved": stage_gbs,
-                               "frac": stage_gbs / peak, "pass1_ms": pass1_ms},
-                     "l2_path": l2_path(w, pass1_ms, pass2_ms, Pl, clocks.get("sm_mhz") or 1900.0)},
+        "roofline": {"bound": "hbm", "kernel": {"pass2_rk2": "pass 2, RK stage 2 (D+-, H, dissipation, RK combine, BRT min)",
+                                                "pass2_rk1": "pass 2, RK stage 1 (D+-, H, dissipation, stage update)",
+                                                "pass2": "pass 2, Euler stage (D+-, H, dissipation, update, BRT min)"}[dom],
+                     "achieved": d["achieved"], "peak": peak, "unit": "GB/s", "frac": d["frac"],
+                     "traffic": d.get("traffic"), "peak_kind": peak_kind, "bytes_per_point": d["bytes_per_point"],
+                     "avg_launch_ms": d["avg_launch_ms"],
+                     "issue": ({"bound_ms": d["issue_bound_ms"], "frac": d["issue_frac"],
+                                "ncu_issue_active": d["ncu_issue_active"],
+                                "note": "warp instructions per launch (ncu) at 1 per SMSP per cycle at the live SM clock"}
+                               if "issue_frac" in d else None),
+                     "kernels": ktab,
+                     "stage": {"bytes_per_point": STAGE_BYTES[key], "ms": stage_ms, "achieved": stage_gbs,
+                               "frac": stage_gbs / peak},
+                     "traffic_source": "profiles/ncu_kernels.json (ncu --set full, one launch per kernel and RK stage)"},
         "clocks": clocks,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": Pl * 4 * world,
                 "d2h_bytes_per_step": Pl * 4 * nout * world},
         "gpu_launches": launches,
-        "kernel_ms_share": {k: v / max(total_ms / args.steps, 1e-9) for k, v in kms.items()},
+        "kernel_ms_share": {k: v / max(total_ms / args.steps, 1e-9) for k, v in kms.items() if k != "pass2_rk2"},
     }
     if args.single_pass_too:
         # the same solve without pass 1 after the first step (alpha^max fixed for a

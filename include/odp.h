@@ -90,7 +90,8 @@ typedef struct {
     double *tau_reached;      /* optional out: tau at return (valid on ODP_ENUMERIC too)            */
     long long *steps_taken;   /* optional out: time steps taken                                     */
     long long *stages_taken;  /* optional out: RK stages evaluated                                  */
-    double *kernel_ms;        /* optional out [3]: summed device time of pass 1, pass 2, finalize   */
+    double *kernel_ms;        /* optional out [4]: summed device time of pass 1, pass 2, finalize,  *
+                               * and of the pass-2 launches of RK stage 2 (included in [1])          */
     int single_pass;          /* 1 -> SURVEY.md §8(f1): when the functor's alpha does not depend on
                                  the derivative range (HOLONOMIC_BOX, DUBINS3D, CAR5D, DOUBLEINT6D)
                                  and the march kernels cover the grid, skip pass 1 after the first

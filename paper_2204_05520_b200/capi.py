@@ -254,7 +254,7 @@ def _opts(cfl, target_ptr, stream_ptr, write_initial, kernel, timing, single_pas
     tr = ctypes.c_double()
     st = ctypes.c_longlong()
     sg = ctypes.c_longlong()
-    km = (ctypes.c_double * 3)()
+    km = (ctypes.c_double * 4)()
     o.tau_reached = ctypes.pointer(tr)
     o.steps_taken = ctypes.pointer(st)
     o.stages_taken = ctypes.pointer(sg)
@@ -270,7 +270,7 @@ def _info(keep, timing, status):
     info = SolveInfo(tau_reached=tr.value, steps=st.value, stages=sg.value, status=status,
                      single_pass=bool(spu.value))
     if timing:
-        info["kernel_ms"] = dict(pass1=km[0], pass2=km[1], control=km[2])
+        info["kernel_ms"] = dict(pass1=km[0], pass2=km[1], control=km[2], pass2_rk2=km[3])
     return info
 
 

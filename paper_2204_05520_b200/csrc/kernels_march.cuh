@@ -56,6 +56,9 @@ namespace odp {
 #ifndef ODP_MARCH_WAIT
 #define ODP_MARCH_WAIT 1       // 1: mbarrier try_wait with a suspend hint; 0: try_wait + nanosleep back-off
 #endif
+#ifndef ODP_MARCH_SLEEP_NS
+#define ODP_MARCH_SLEEP_NS 64   // back-off of the ODP_MARCH_WAIT = 0 wait loop
+#endif
 #ifndef ODP_MARCH_SELP
 #define ODP_MARCH_SELP 0       // 1: ENO pick as FSET + 3 FMA-pipe ops instead of FSETP + FSEL
 #endif
@@ -314,6 +317,8 @@ struct MarchArgs {
     int side_off;         // float offset of the side buffers
     int bar_off;          // float offset of the mbarriers
     int tab_off;          // float offset of the per-unit copy table
+    int aux_off;          // float offset of the per-warp side geometry [16][2*3] and the marching coordinate table
+    int mtab_n;           // entries of the marching coordinate table in shared memory (0: read the global table)
     int sn[3];            // local extents of the side axes (work order, march_col)
     int b1;               // axis-1 block of the work order (divides sn[1])
     int ncols;            // columns (product of the side extents)
@@ -414,7 +419,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) 
         "selp.u32 %0, 1, 0, p;\n}"
         : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
     while (!ok) {
-        __nanosleep(64);
+        __nanosleep(ODP_MARCH_SLEEP_NS);
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -585,6 +590,29 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
         if (nbw0) tma_bulk_g2s_u32(smem_u32(slot + RMG), W + tt + t_ring[6], nbw0, bar);
         if (nbw1) tma_bulk_g2s_u32(smem_u32(slot + t_ring[5]), W + tt, nbw1, bar);
     };
+    // per-warp side geometry (index and extent per side axis, read only on face columns) and the
+    // marching axis' coordinate tables (x, cos, sin) staged once per launch
+    int *wgeo = reinterpret_cast<int *>(smem + a.aux_off) + (tid >> 5) * 6;
+    float *mtab = smem + a.aux_off + 96;
+    if constexpr (PASS2) {
+        if (((F::NEED_X | F::NEED_TRIG) >> MA) & 1)
+            for (int jj = tid; jj < a.mtab_n; jj += blockDim.x) {
+                if ((F::NEED_X >> MA) & 1) mtab[jj] = __ldg(g.tab + g.tab_off[MA] + jj);
+                if ((F::NEED_TRIG >> MA) & 1) {
+                    mtab[a.mtab_n + jj] = __ldg(g.tab + g.tab_off[MA] + g.Ng[MA] + jj);
+                    mtab[2 * a.mtab_n + jj] = __ldg(g.tab + g.tab_off[MA] + 2 * g.Ng[MA] + jj);
+                }
+            }
+    }
+    auto load_march = [&](Pt &q, int jg) {            // coordinates of the marching axis at global index jg
+        if (a.mtab_n) {
+            if ((F::NEED_X >> MA) & 1) q.x[MA] = mtab[jg];
+            if ((F::NEED_TRIG >> MA) & 1) { q.c[MA] = mtab[a.mtab_n + jg]; q.s[MA] = mtab[2 * a.mtab_n + jg]; }
+        } else {
+            load_axis<F>(g, q, MA, jg);
+        }
+    };
+
     if (tid == 0) {
         for (int b = 0; b < NST; ++b) {
             mbar_init(&tmab[b], 1);
@@ -648,9 +676,15 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
             const bool rface = !a.per2 && (grow < R || grow > N2 - 1 - R);   // ghost rows in the row window
             int oid[NSA], oN[NSA];
             side_geom(U.col, oid, oN);
-            bool oface[NSA];
+            uint32_t fmask = 0;                               // bit o: the column is within R of a face of side axis o
 #pragma unroll
-            for (int o = 0; o < MA; ++o) oface[o] = !g.per[o] && (oid[o] < R || oid[o] > oN[o] - 1 - R);
+            for (int o = 0; o < MA; ++o)
+                if (!g.per[o] && (oid[o] < R || oid[o] > oN[o] - 1 - R)) fmask |= 1u << o;
+            __syncwarp();
+            if ((tid & 31) == 0)
+#pragma unroll
+                for (int o = 0; o < MA; ++o) { wgeo[2 * o] = oid[o]; wgeo[2 * o + 1] = oN[o]; }
+            __syncwarp();
             Pt qrow;
             if constexpr (PASS2) {
 #pragma unroll
@@ -714,7 +748,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                     Pt q0;
                     if constexpr (PASS2) {
                         q0 = qrow;
-                        load_axis<F>(g, q0, MA, jg);
+                        load_march(q0, jg);
                     }
                     float2 acc = f2s(0.f), dis = f2s(0.f);
                     float2 pv[F::SEPARABLE ? 1 : NDIM];     // costate of the node pair (non-separable H)
@@ -767,12 +801,13 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
 #pragma unroll
                     for (int o = 0; o < MA; ++o) {
                         const uint32_t so = sbs + (uint32_t)(o * 2 * R * SSZ * 4);
-                        if (PASS2 || oface[o]) {
+                        const bool of = (fmask >> o) & 1u;
+                        if (PASS2 || of) {
                             float2 x[2 * R + 1];
 #pragma unroll
                             for (int k = -R; k <= R; ++k)
                                 x[k + R] = k == 0 ? v0 : lds2(so + (uint32_t)((k < 0 ? k + R : k + R - 1) * SSZ * 4));
-                            if (oface[o]) fix_ghosts2<R>(x, oid[o], oN[o]);
+                            if (of) fix_ghosts2<R>(x, wgeo[2 * o], wgeo[2 * o + 1]);
                             float2 uu, ww, mr, d1r;
                             classic(x, uu, ww, mr, d1r);
                             if constexpr (PASS2) {
@@ -780,7 +815,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                             } else {
                                 inc_val(uu, mn[o], mx[o]);
                                 inc_val(ww, mn[o], mx[o]);
-                                if (R == 2 && oid[o] + 1 <= oN[o] - 1) inc_val(fma2(f2s(0.5f), mr, d1r), mn[o], mx[o]);   // D-_{i+1}
+                                if (R == 2 && wgeo[2 * o] + 1 <= wgeo[2 * o + 1] - 1) inc_val(fma2(f2s(0.5f), mr, d1r), mn[o], mx[o]);   // D-_{i+1}
                             }
                         } else {
                             // pass 1, interior: the node's upper edge i+1/2 (both sides)
@@ -1068,6 +1103,11 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     a.side_off = geo_side_off(R, N1, best, nst);
     a.bar_off = geo_bar_off(R, N1, best, NSS, nst);
     a.tab_off = a.bar_off + 36;                     // 2 NST + R + NST + NST <= 18 mbarriers (144 B)
+    a.aux_off = a.tab_off + 112;                    // copy table (64 + 32 + 8 + 4 floats) rounded
+    {
+        const int NmG = MA == 0 ? g.Ng0 : g.N[MA];
+        a.mtab_n = NmG <= 1024 ? NmG : 0;
+    }
     for (int o = 0; o < 3; ++o) a.sn[o] = o < MA ? g.N[o] : 1;
     a.b1 = 1;
     if (MA == 3) {
@@ -1096,7 +1136,8 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     a.i0map = 0; a.i0r = 0; a.s0n = a.sn[0];
     a.wslot = 0;                                    // pass 2 launches use slot 1 (march_pass2)
     p->block = ((a.nthr + 31) / 32) * 32 + 32;      // compute warps + the producer warp
-    p->smem = (size_t)geo_smem_bytes(R, N1, best, NSS, nst);
+    p->smem = (size_t)(a.aux_off + 96 + 3 * a.mtab_n) * 4;
+    p->smem = std::max(p->smem, (size_t)geo_smem_bytes(R, N1, best, NSS, nst));
     p->grid = 0;
     return true;
 }

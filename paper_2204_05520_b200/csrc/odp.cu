@@ -981,7 +981,7 @@ static odp_status validate(const odp_grid *g, int dyn, const double *params, int
 
 namespace {
 struct Launch {
-    int kind;          // 0 pass1, 1 pass2, 2 finalize/control
+    int kind;          // 0 pass1, 1 pass2, 2 finalize/control, 3 pass2 of RK stage 2
     int ev;            // index of the start event (stop = ev + 1), -1 if untimed
 };
 }
@@ -1071,7 +1071,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
     const float *T = (opts && opts->target) ? opts->target : V0;
     const int write_initial = opts ? opts->write_initial : 0;
     const bool timed = opts && opts->kernel_ms;
-    double kms[3] = {0, 0, 0};
+    double kms[4] = {0, 0, 0, 0};       // pass 1, pass 2, control, pass 2 of RK stage 2 (subset of pass 2)
 
     FParams fp;
     memset(&fp, 0, sizeof fp);
@@ -1202,7 +1202,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
                 if ((r = rec(1, [&] { launch_pass2(buf[0], nullptr, buf[1], STAGE_RK1, true); }))) return r;
                 if ((r = rec(2, [&] { launch_guard(0); }))) return r;
                 if (g->nranks > 1 && (r = rec(2, [&] { exch(buf[1]); }))) return r;
-                if ((r = rec(1, [&] { launch_pass2(buf[1], buf[0], buf[0], STAGE_RK2, true); }))) return r;
+                if ((r = rec(3, [&] { launch_pass2(buf[1], buf[0], buf[0], STAGE_RK2, true); }))) return r;
                 if ((r = rec(2, [&] { launch_guard(1); }))) return r;
             }
         } else if (accuracy == ODP_LOW) {
@@ -1215,7 +1215,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
             if ((r = rec(1, [&] { launch_pass2(buf[0], nullptr, buf[1], STAGE_RK1); }))) return r;
             if ((r = exch_pass1(buf[1]))) return r;
             if ((r = rec(2, [&] { launch_fin(1, 0); }))) return r;
-            if ((r = rec(1, [&] { launch_pass2(buf[1], buf[0], buf[0], STAGE_RK2); }))) return r;
+            if ((r = rec(3, [&] { launch_pass2(buf[1], buf[0], buf[0], STAGE_RK2); }))) return r;
         }
         return rec(2, [&] { k_advance<<<1, 1, 0, s>>>(g->d_state); });
     };
@@ -1291,7 +1291,8 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
                     if (step_of_launch[q] >= done) continue;      // launches that found the interval done
                     float ms = 0.f;
                     CUDA_TRY(cudaEventElapsedTime(&ms, g->events[launches[q].ev], g->events[launches[q].ev + 1]));
-                    kms[launches[q].kind] += ms;
+                    kms[launches[q].kind == 3 ? 1 : launches[q].kind] += ms;
+                    if (launches[q].kind == 3) kms[3] += ms;
                 }
             }
             if (g->h_state->status) { rs = ODP_ENUMERIC; break; }
@@ -1328,7 +1329,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
         if (opts->tau_reached) *opts->tau_reached = g->h_state->tau;
         if (opts->steps_taken) *opts->steps_taken = g->h_state->steps;
         if (opts->stages_taken) *opts->stages_taken = g->h_state->stages;
-        if (opts->kernel_ms) for (int q = 0; q < 3; ++q) opts->kernel_ms[q] = kms[q];
+        if (opts->kernel_ms) for (int q = 0; q < 4; ++q) opts->kernel_ms[q] = kms[q];
         if (opts->single_pass_used) *opts->single_pass_used = single ? 1 : 0;
     }
     if (rs == ODP_ENUMERIC)
