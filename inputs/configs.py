@@ -212,6 +212,16 @@ def make_v0(w: Workload, seed: Optional[int] = None, noise: float = 1e-3, i0=Non
     box = [(begin, count) per axis] returns the sub-box -- bitwise the same values as slicing the
     whole array (the windowed checks of pin Z12 build only the boxes they need; unseeded only).
     """
+    if seed is None and box is None:
+        # large requests (a c5 rank slab is up to 8e9 points): build the float32 result an axis-0
+        # plane at a time, so the float64 intermediate stays one plane (bitwise the same values)
+        b0, c0 = (0, w.N[0]) if i0 is None else (int(i0[0]), int(i0[1]))
+        plane = int(np.prod(w.N[1:], dtype=np.int64))
+        if c0 * plane > (1 << 26) and c0 > 1:
+            out = np.empty((c0,) + tuple(w.N[1:]), dtype=np.float32)
+            for k in range(c0):
+                out[k] = make_v0(w, box=[(b0 + k, 1)] + [(0, n) for n in w.N[1:]])[0]
+            return out
     axes = [axis_nodes(n, l, h, bool(p)) for n, l, h, p in zip(w.N, w.lo, w.hi, w.periodic)]
     kind = w.target[0]
     shape = w.N

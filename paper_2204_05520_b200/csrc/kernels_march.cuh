@@ -128,8 +128,30 @@ __device__ __forceinline__ void inc_s(float v, float &mn, float &mx) {
     mx = fmaxf(mx, v);
 }
 
+// ---- ODP_CHECK builds (libodp_check.so, tests/test_gpu_checked.py): device-side bounds and
+// alignment checks of every shared-memory read, TMA copy and global access of the march kernels,
+// in place of compute-sanitizer (closed on this pool).  A failed check prints and traps. ----------
+#ifdef ODP_CHECK
+extern __shared__ __align__(128) float odp_dyn_smem[];
+__device__ __noinline__ void odp_check_fail(int code, long long a, long long b) {
+    printf("odp check %d failed: %lld %lld (block %d thread %d)\n", code, a, b, blockIdx.x, threadIdx.x);
+    __trap();
+}
+#define ODP_CHK(cond, code, a, b) do { if (!(cond)) odp_check_fail((code), (long long)(a), (long long)(b)); } while (0)
+__device__ __forceinline__ void odp_chk_smem(uint32_t addr, uint32_t bytes, int code) {
+    uint32_t dsz;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsz));
+    const uint32_t base = smem_u32(odp_dyn_smem);
+    ODP_CHK(addr >= base && addr + bytes <= base + dsz && (addr & (bytes >= 8 ? 7u : 3u)) == 0, code, addr - base, dsz);
+}
+#else
+#define ODP_CHK(cond, code, a, b) ((void)0)
+__device__ __forceinline__ void odp_chk_smem(uint32_t, uint32_t, int) {}
+#endif
+
 // 8-byte shared-memory load at a 32-bit shared address (one base register + immediate offsets)
 __device__ __forceinline__ float2 lds2(uint32_t addr) {
+    odp_chk_smem(addr, 8, 1);
     float2 v;
     asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
     return v;
@@ -583,6 +605,21 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
             }
         }
         if (a.dbg & 4) nb = nbw0 = nbw1 = 0;          // experiment: no data movement (garbage tiles)
+#ifdef ODP_CHECK
+        {
+            const long long wlo = -2LL * g.stride[0], whi = g.P + 2LL * g.stride[0];   // W: local planes + 2 halo planes
+            auto chk_copy = [&](uint32_t d, const float *sp, uint32_t n, int code) {
+                if (!n) return;
+                const long long e = sp - W;
+                ODP_CHK(e >= wlo && e + n / 4 <= whi, code, e, n);
+                ODP_CHK(((uintptr_t)sp & 15) == 0 && (d & 15) == 0 && (n & 15) == 0, code + 1, (long long)(uintptr_t)sp, n);
+                odp_chk_smem(d, n, code + 2);
+            };
+            chk_copy(dst, src, nb, 10);
+            if (nbw0) chk_copy(smem_u32(slot + RMG), W + tt + t_ring[6], nbw0, 20);
+            if (nbw1) chk_copy(smem_u32(slot + t_ring[5]), W + tt, nbw1, 30);
+        }
+#endif
         const uint32_t total = __reduce_add_sync(0xffffffffu, nb + nbw0 + nbw1);
         if (lane == 0) mbar_expect_tx(bar, total);
         __syncwarp();
@@ -699,7 +736,11 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
             if (act) {
                 float2 x[2 * R + 1];
 #pragma unroll
-                for (int k = -R; k <= R; ++k) x[k + R] = __ldg(reinterpret_cast<const float2 *>(cb + (long long)mloc(m0 + k) * M));
+                for (int k = -R; k <= R; ++k) {
+                    ODP_CHK(cb + (long long)mloc(m0 + k) * M - W >= -2LL * g.stride[0] &&
+                            cb + (long long)mloc(m0 + k) * M - W + 2 <= g.P + 2LL * g.stride[0], 40, m0 + k, 0);
+                    x[k + R] = __ldg(reinterpret_cast<const float2 *>(cb + (long long)mloc(m0 + k) * M));
+                }
                 if (!mper && (m0 < R || m0 > Nm - 1 - R)) fix_ghosts2<R>(x, m0, Nm);
 #pragma unroll
                 for (int k = 0; k < R; ++k) win[k] = x[R + k];
@@ -717,6 +758,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
             if constexpr (PASS2) {
                 if (act) {
                     const long long gi0 = U.cbase + (long long)(m0 - mlo) * M + grow * N1 + qc0;
+                    ODP_CHK(gi0 >= 0 && gi0 + 2 <= g.P, 41, gi0, g.P);
                     if (kind == STAGE_RK2) vnv = *reinterpret_cast<const float2 *>(Vn + gi0);
                     if (brt && kind != STAGE_RK1) ttv = __ldg(reinterpret_cast<const float2 *>(T + gi0));
                 }
@@ -730,6 +772,8 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                 float2 vin = f2s(0.f);
                 if (act && !in_ring) {
                     if (mper || kin < Nm) {
+                        ODP_CHK(cb + (long long)mloc(kin) * M - W >= -2LL * g.stride[0] &&
+                                cb + (long long)mloc(kin) * M - W + 2 <= g.P + 2LL * g.stride[0], 43, kin, 0);
                         vin = __ldg(reinterpret_cast<const float2 *>(cb + (long long)mloc(kin) * M));
                     } else {                                  // beyond the high face: ghost (A12)
                         const float2 e = __ldg(reinterpret_cast<const float2 *>(cb + (long long)(Nm - 1 - mlo) * M));
@@ -929,6 +973,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                         float2 v = fma2(f2s(dt), L, v0);                        // W + dt L
                         if (kind == STAGE_RK2) v = mul2(f2s(0.5f), add2(vnv, v));  // (Vn + V2)/2 (A10)
                         if (brt && kind != STAGE_RK1) v = f2(fminf(v.x, ttv.x), fminf(v.y, ttv.y));
+                        ODP_CHK(gi >= 0 && gi + 2 <= g.P, 42, gi, g.P);
                         *reinterpret_cast<float2 *>(out + gi) = v;
                         mabs = max3nan(mabs, fabsf(v.x), fabsf(v.y));   // output guard (single-pass solves)
                         if (jg + 1 < m1) {                    // the next step's Vn / target

@@ -360,6 +360,13 @@ __global__ void __launch_bounds__(TTR_TX * TTR_TY) k_ttr_tile(GridDev g, FParams
     auto issue = [&](uint32_t sb, const float *pl) {
 #pragma unroll
         for (int k = 0; k < NE; ++k)
+#ifdef ODP_CHECK
+            if (eok[k] && !(pl + eoff[k] - src >= 0 && pl + eoff[k] - src < g.P)) {
+                printf("odp check 60 failed: ttr tile source %lld of %lld (block %d)\n", (long long)(pl + eoff[k] - src),
+                       (long long)g.P, blockIdx.x);
+                __trap();
+            } else
+#endif
             if (eok[k])
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sb + 4u * (uint32_t)(threadIdx.x + k * NT)),
                              "l"(pl + eoff[k]) : "memory");
