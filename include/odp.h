@@ -65,16 +65,24 @@ typedef enum {
 
 /* Kernel family used for the two passes of every stage. */
 typedef enum {
-    ODP_KERNEL_AUTO = 0,     /* march, else stream, else tiled, else generic -- the first that
-                                covers the grid                                                */
+    ODP_KERNEL_AUTO = 0,     /* resident on small grids (below), else march, else stream, else
+                                tiled, else generic -- the first that covers the grid          */
     ODP_KERNEL_GENERIC = 1,  /* one thread per node, neighbours through L1/L2                 */
     ODP_KERNEL_TILED = 2,    /* inner-plane tile + every outer neighbour tile staged in shared
                                 memory by 1-D TMA bulk copies (mbarrier pipeline)             */
     ODP_KERNEL_STREAM = 3,   /* CTA marches the innermost outer axis with a register window;
                                 in-plane tile in padded shared memory                          */
-    ODP_KERNEL_MARCH = 4     /* the stream decomposition with edge-shared ENO2 picks carried
+    ODP_KERNEL_MARCH = 4,    /* the stream decomposition with edge-shared ENO2 picks carried
                                 along the marching axis, edge-assigned pass 1, packed FP32x2
                                 arithmetic and one barrier per step (kernels_march.cuh)       */
+    ODP_KERNEL_RESIDENT = 5  /* small grids: the WHOLE solve (every interval, step, stage,
+                                finalize and snapshot) in one cooperative launch with grid
+                                barriers between the passes; the generic per-node arithmetic
+                                (bitwise the generic family's result).  AUTO picks it on one
+                                rank for grids up to 2^18 nodes (env ODP_RESIDENT_MAX_POINTS)
+                                unless kernel_ms or single_pass is requested.  Not for
+                                PAIR_DUBINS3D (alpha^max over three axes).  ODP_EINVAL when
+                                requested where it does not apply.                             */
 } odp_kernel;
 
 typedef struct odp_grid odp_grid;   /* opaque; one solve at a time per handle */

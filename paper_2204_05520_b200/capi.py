@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("ODP_LIB_PATH") or os.path.join(HERE, "libodp.so")
 ODP_OK, ODP_EINVAL, ODP_ENUMERIC, ODP_ECUDA, ODP_ENCCL, ODP_ENOMEM = 0, 1, 2, 3, 4, 5
 ACCURACY = {"low": 1, "medium": 2}
 MODE = {"brs": 0, "brt": 1}
-KERNEL = {"auto": 0, "generic": 1, "tiled": 2, "stream": 3, "march": 4}
+KERNEL = {"auto": 0, "generic": 1, "tiled": 2, "stream": 3, "march": 4, "resident": 5}
 DYNAMICS = {"HOLONOMIC_BALL": 0, "HOLONOMIC_BOX": 1, "DUBINS3D": 2, "CAR4D": 3, "CAR5D": 4, "DOUBLEINT6D": 5,
             "PAIR_DUBINS3D": 6}
 

@@ -44,10 +44,16 @@ __device__ __forceinline__ void block_reduce_range(float *mn, float *mx, float m
     }
 }
 
+// Load of a value array: through the non-coherent path for the launch-per-pass kernels (W is
+// read-only for the launch), through L2 (ld.global.cg) inside k_resident, where the arrays are
+// rewritten between the grid barriers of one launch.
+template <bool CG>
+__device__ __forceinline__ float ldw(const float *p) { return CG ? __ldcg(p) : __ldg(p); }
+
 // Value of W at offset k (|k| <= R) from local node `i` (flat index) along axis d, whose index on
 // that axis is `id` (local).  Periodic axes wrap; non-periodic out-of-domain slots are left for
 // fix_ghosts.  Axis 0 consults the global index so halo planes of a slab are used.
-template <int R>
+template <int R, bool CG = false>
 __device__ __forceinline__ void load_line(const GridDev &g, const float *__restrict__ W, long long i, int d,
                                           int id, float *v) {
     const long long s = g.stride[d];
@@ -56,8 +62,8 @@ __device__ __forceinline__ void load_line(const GridDev &g, const float *__restr
 #pragma unroll
         for (int k = -R; k <= R; ++k) {
             const int gj = gid + k;
-            if (gj >= 0 && gj < g.Ng0) v[k + R] = __ldg(W + i + k * s);
-            else if (g.per[0]) { int w = gj < 0 ? gj + g.Ng0 : gj - g.Ng0; v[k + R] = __ldg(W + i + (long long)(w - gid) * s); }
+            if (gj >= 0 && gj < g.Ng0) v[k + R] = ldw<CG>(W + i + k * s);
+            else if (g.per[0]) { int w = gj < 0 ? gj + g.Ng0 : gj - g.Ng0; v[k + R] = ldw<CG>(W + i + (long long)(w - gid) * s); }
             else v[k + R] = 0.f;
         }
         if (!g.per[0]) fix_ghosts<R>(v, gid, g.Ng0);
@@ -67,8 +73,8 @@ __device__ __forceinline__ void load_line(const GridDev &g, const float *__restr
 #pragma unroll
     for (int k = -R; k <= R; ++k) {
         const int j = id + k;
-        if (j >= 0 && j < N) v[k + R] = __ldg(W + i + k * s);
-        else if (g.per[d]) { int w = j < 0 ? j + N : j - N; v[k + R] = __ldg(W + i + (long long)(w - id) * s); }
+        if (j >= 0 && j < N) v[k + R] = ldw<CG>(W + i + k * s);
+        else if (g.per[d]) { int w = j < 0 ? j + N : j - N; v[k + R] = ldw<CG>(W + i + (long long)(w - id) * s); }
         else v[k + R] = 0.f;
     }
     if (!g.per[d]) fix_ghosts<R>(v, id, N);
@@ -76,7 +82,7 @@ __device__ __forceinline__ void load_line(const GridDev &g, const float *__restr
 
 template <int NDIM>
 __device__ __forceinline__ void node_index(const GridDev &g, long long i, int *idx) {
-    long long r = i / g.stride[0];
+    const long long r = (g.P <= 0x7fffffffLL) ? (long long)((unsigned)i / (unsigned)g.stride[0]) : i / g.stride[0];
     idx[0] = (int)r;
     int rem = (int)(i - r * g.stride[0]);
 #pragma unroll
@@ -86,9 +92,10 @@ __device__ __forceinline__ void node_index(const GridDev &g, long long i, int *i
     }
 }
 
-template <int NDIM, int R>
-__global__ void __launch_bounds__(256) k_pass1_generic(GridDev g, const float *__restrict__ W, float *partials,
-                                                       const DevState *st) {
+// Pass 1 of one stage over all nodes, grid-stride; st may point to a CTA-local (shared) copy.
+template <int NDIM, int R, bool CG>
+__device__ __forceinline__ void pass1_generic_body(const GridDev &g, const float *__restrict__ W, float *partials,
+                                                   const DevState *st) {
     if (!st->active) return;
     float mn[NDIM], mx[NDIM];
 #pragma unroll
@@ -99,13 +106,13 @@ __global__ void __launch_bounds__(256) k_pass1_generic(GridDev g, const float *_
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.P; i += stride) {
         int idx[NDIM];
         node_index<NDIM>(g, i, idx);
-        const float w = __ldg(W + i);
+        const float w = ldw<CG>(W + i);
         nan |= (w != w);
         mabs = fmaxf(mabs, fabsf(w));
 #pragma unroll
         for (int d = 0; d < NDIM; ++d) {
             float v[2 * R + 1], dm, dp;
-            load_line<R>(g, W, i, d, idx[d], v);
+            load_line<R, CG>(g, W, i, d, idx[d], v);
             deriv<R>(v, g.inv_dx[d], dm, dp);
             mn[d] = fminf(mn[d], fminf(dm, dp));
             mx[d] = fmaxf(mx[d], fmaxf(dm, dp));
@@ -114,11 +121,17 @@ __global__ void __launch_bounds__(256) k_pass1_generic(GridDev g, const float *_
     block_reduce_range<NDIM>(mn, mx, mabs, nan, partials);
 }
 
-template <class F, int NDIM, int R>
-__global__ void __launch_bounds__(256) k_pass2_generic(GridDev g, const float *__restrict__ W,
-                                                       const float *Vn, const float *__restrict__ T,
-                                                       float *out, const DevState *st, FParams fp,
-                                                       int kind, int brt) {
+template <int NDIM, int R>
+__global__ void __launch_bounds__(256) k_pass1_generic(GridDev g, const float *__restrict__ W, float *partials,
+                                                       const DevState *st) {
+    pass1_generic_body<NDIM, R, false>(g, W, partials, st);
+}
+
+// Pass 2 of one stage over all nodes, grid-stride; st may point to a CTA-local (shared) copy.
+template <class F, int NDIM, int R, bool CG>
+__device__ __forceinline__ void pass2_generic_body(const GridDev &g, const float *__restrict__ W, const float *Vn,
+                                                   const float *__restrict__ T, float *out, const DevState *st,
+                                                   const FParams &fp, int kind, int brt) {
     if (!st->active) return;
     F f;
     f.init(fp, st->minD, st->maxD);
@@ -134,15 +147,23 @@ __global__ void __launch_bounds__(256) k_pass2_generic(GridDev g, const float *_
 #pragma unroll
         for (int d = 0; d < NDIM; ++d) {
             float v[2 * R + 1];
-            load_line<R>(g, W, i, d, idx[d], v);
+            load_line<R, CG>(g, W, i, d, idx[d], v);
             deriv<R>(v, g.inv_dx[d], dm[d], dp[d]);
             p[d] = 0.5f * (dm[d] + dp[d]);                 // A3
         }
         float L = f.ham(q, p);                              // l.154-156
 #pragma unroll
         for (int d = 0; d < NDIM; ++d) L = fmaf(f.alpha(d, q), 0.5f * (dp[d] - dm[d]), L);   // l.163 (A2)
-        out[i] = stage_update(kind, brt, __ldg(W + i), L, dt, Vn, T, i);
+        out[i] = stage_update(kind, brt, ldw<CG>(W + i), L, dt, Vn, T, i);
     }
+}
+
+template <class F, int NDIM, int R>
+__global__ void __launch_bounds__(256) k_pass2_generic(GridDev g, const float *__restrict__ W,
+                                                       const float *Vn, const float *__restrict__ T,
+                                                       float *out, const DevState *st, FParams fp,
+                                                       int kind, int brt) {
+    pass2_generic_body<F, NDIM, R, false>(g, W, Vn, T, out, st, fp, kind, brt);
 }
 
 }  // namespace odp

@@ -142,11 +142,14 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const float *__restrict
     }
 }
 
-template <class F, int NDIM>
-__global__ void __launch_bounds__(256) k_finalize(const float *__restrict__ partials, int nparts, DevState *st,
-                                                  GridDev g, FParams fp, const double *__restrict__ dxd,
-                                                  int stage_in_step, int final_check, const float *__restrict__ range,
-                                                  const float *__restrict__ amax_parts, int namax) {
+// The body of k_finalize; k_resident runs it in every CTA on a CTA-local copy of the state (CG:
+// partials read through L2, they are rewritten between the grid barriers of that launch).
+template <class F, int NDIM, bool CG>
+__device__ __forceinline__ void finalize_body(const float *partials, int nparts, DevState *st,
+                                              const GridDev &g, const FParams &fp, const double *__restrict__ dxd,
+                                              int stage_in_step, int final_check, const float *__restrict__ range,
+                                              const float *__restrict__ amax_parts, int namax,
+                                              bool reuse_amax = false) {
     if (!st->active) return;
     constexpr int Q = 2 * NDIM + 2;
     __shared__ float red[Q][8];
@@ -156,19 +159,28 @@ __global__ void __launch_bounds__(256) k_finalize(const float *__restrict__ part
     if (range) {            // multi-GPU: the range record was allreduced over the ranks
         if (threadIdx.x < Q) rng[threadIdx.x] = threadIdx.x < NDIM ? -range[threadIdx.x] : range[threadIdx.x];
     } else
-    // reduce the per-CTA partials of pass 1 (min/max are exact: any order gives the same bits)
-    for (int q = 0; q < Q; ++q) {
-        float r = q < NDIM ? __int_as_float(0x7f800000) : (q < 2 * NDIM ? -__int_as_float(0x7f800000) : 0.f);
+    // reduce the per-CTA partials of pass 1 (min/max are exact: any order gives the same bits);
+    // all Q entries of a record are loaded before any reduction so the loads overlap
+    {
+        float r[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) r[q] = q < NDIM ? __int_as_float(0x7f800000) : (q < 2 * NDIM ? -__int_as_float(0x7f800000) : 0.f);
         for (int p = threadIdx.x; p < nparts; p += blockDim.x) {
-            const float o = partials[(long long)p * Q + q];
-            r = q < NDIM ? fminf(r, o) : fmaxf(r, o);
+            float o[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) o[q] = ldw<CG>(partials + (long long)p * Q + q);
+#pragma unroll
+            for (int q = 0; q < Q; ++q) r[q] = q < NDIM ? fminf(r[q], o[q]) : fmaxf(r[q], o[q]);
         }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const float o = __shfl_xor_sync(0xffffffffu, r, off);
-            r = q < NDIM ? fminf(r, o) : fmaxf(r, o);
+        for (int q = 0; q < Q; ++q) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const float o = __shfl_xor_sync(0xffffffffu, r[q], off);
+                r[q] = q < NDIM ? fminf(r[q], o) : fmaxf(r[q], o);
+            }
+            if (lane == 0) red[q][warp] = r[q];
         }
-        if (lane == 0) red[q][warp] = r;
     }
     __syncthreads();
     if (!range && threadIdx.x < Q) {
@@ -195,7 +207,10 @@ __global__ void __launch_bounds__(256) k_finalize(const float *__restrict__ part
     F f;
     f.init(fp, rng, rng + NDIM);
     __shared__ float am[NDIM];
-    if constexpr (F::DEPS3) {   // alpha_d depends on 3 coordinates: per-CTA maxima from k_amax3
+    if (F::RANGE_FREE && reuse_amax) {   // k_resident: alpha^max of a RANGE_FREE functor is the
+        if (threadIdx.x < NDIM) am[threadIdx.x] = st->amax[threadIdx.x];   // previous step's, bit for bit
+        __syncthreads();
+    } else if constexpr (F::DEPS3) {   // alpha_d depends on 3 coordinates: per-CTA maxima from k_amax3
         if (threadIdx.x < NDIM) {
             float a = 0.f;
             for (int p = 0; p < namax; ++p) a = fmaxf(a, amax_parts[p * NDIM + threadIdx.x]);
@@ -237,6 +252,15 @@ __global__ void __launch_bounds__(256) k_finalize(const float *__restrict__ part
     }
 }
 
+template <class F, int NDIM>
+__global__ void __launch_bounds__(256) k_finalize(const float *__restrict__ partials, int nparts, DevState *st,
+                                                  GridDev g, FParams fp, const double *__restrict__ dxd,
+                                                  int stage_in_step, int final_check, const float *__restrict__ range,
+                                                  const float *__restrict__ amax_parts, int namax) {
+    finalize_body<F, NDIM, false>(partials, nparts, st, g, fp, dxd, stage_in_step, final_check, range, amax_parts,
+                                  namax);
+}
+
 __global__ void k_init_state(DevState *st, double cfl, double eps) {
     st->tau = 0.0; st->tau_target = 0.0; st->eps = eps; st->dt = 0.0; st->cfl = cfl; st->dt_f = 0.f;
     st->maxabs = 0.f; st->nan = 0; st->active = 0; st->status = 0; st->steps = 0; st->stages = 0; st->pending = 0;
@@ -244,16 +268,18 @@ __global__ void k_init_state(DevState *st, double cfl, double eps) {
     for (int d = 0; d < MAXD; ++d) { st->minD[d] = 0.f; st->maxD[d] = 0.f; st->amax[d] = 0.f; }
 }
 
-__global__ void k_begin(DevState *st, double tau_k) {
+__device__ __forceinline__ void begin_body(DevState *st, double tau_k) {
     if (st->pending) { st->status = ODP_ENUMERIC; st->pending = 0; }
     st->tau_target = tau_k;
     st->active = (st->status == 0 && tau_k - st->tau > st->eps) ? 1 : 0;
 }
+__global__ void k_begin(DevState *st, double tau_k) { begin_body(st, tau_k); }
 
-__global__ void k_force_active(DevState *st) {
+__device__ __forceinline__ void force_active_body(DevState *st) {
     if (st->pending) { st->status = ODP_ENUMERIC; st->pending = 0; }
     st->active = st->status == 0 ? 1 : 0;
 }
+__global__ void k_force_active(DevState *st) { force_active_body(st); }
 
 // For functors whose alpha_d depends on three coordinates (DEPS3, e.g. Eq. 7): the stage's range is
 // stored first (k_store_range: the same exact min/max reduction as k_finalize), then k_amax3 takes
@@ -386,11 +412,120 @@ __global__ void __launch_bounds__(256) k_guard(const float *__restrict__ partial
     }
 }
 
-__global__ void k_advance(DevState *st) {                               // O8: tau += dt (float64)
+__device__ __forceinline__ void advance_body(DevState *st) {           // O8: tau += dt (float64)
     if (!st->active) return;
     st->tau += st->dt;
     st->steps += 1;
     if (st->tau_target - st->tau <= st->eps) st->active = 0;
+}
+__global__ void k_advance(DevState *st) { advance_body(st); }
+
+// ------------------------------------------------------------------------------------------------
+// k_resident: the whole solve of a small grid in ONE cooperative launch (ODP_KERNEL_RESIDENT).
+// A grid that fits in L2 many times over (c1: 61k nodes, 242 KB per array) spends its time on
+// launch gaps and host round trips, not on HBM: ~10 launches per step and a D2H + host sync per
+// save interval, each a few us, against ~1 us of arithmetic per pass.  Here every save interval,
+// time step, RK stage, finalize and snapshot runs inside one kernel: the passes are the generic
+// family's per-node bodies (so the result is bitwise the generic family's: same arithmetic per
+// node, min/max partials exact in any order), arrays read through L2 (ld.global.cg), and the
+// control kernels (k_begin, k_finalize, k_advance, k_force_active) run redundantly in EVERY CTA
+// on a CTA-local copy of DevState -- same inputs, same float64 operations, so every copy takes
+// the same decisions and the only grid-wide synchronisation is one barrier after each pass.
+// CTA 0 writes the state back at the end.  Launched with cudaLaunchCooperativeKernel (all CTAs
+// co-resident, required by the spin barrier).
+// ------------------------------------------------------------------------------------------------
+struct ResidentArgs {
+    float *buf0, *buf1;          // V ping-pong (local slab layout, no halo use: one rank)
+    const float *T;              // BRT target
+    float *out;                  // snapshots, out + k * P
+    const double *tau;           // device copy of the save times
+    int ntau, k_out0;
+    float *partials;             // gridDim.x * (2n + 2) floats
+    const double *dxd;
+    DevState *st;
+    unsigned *bar;               // grid barrier counter, zeroed before the launch
+    int low, brt;
+};
+
+// Grid-wide barrier: monotonic arrival counter, CTA b waits until gen * gridDim.x arrivals.  The
+// __syncthreads + gpu-scope fence before the arrival release the CTA's writes; the acquire load
+// orders the reads after it.
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &gen) {
+    __syncthreads();
+    gen += 1;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        const unsigned target = gen * gridDim.x;
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while ((int)(v - target) < 0);
+    }
+    __syncthreads();
+}
+
+template <class F, int NDIM, int R>
+__global__ void __launch_bounds__(256) k_resident(GridDev g, FParams fp, ResidentArgs a) {
+    __shared__ DevState sst;
+    if (threadIdx.x == 0) sst = *a.st;
+    __syncthreads();
+    unsigned gen = 0;
+    float *buf[2] = {a.buf0, a.buf1};
+    const long long P = g.P;
+    const int np = gridDim.x;
+    int cur = 0, k_out = a.k_out0;
+    auto ctl = [&](auto &&fn) {                 // one control step on the CTA-local state
+        __syncthreads();
+        if (threadIdx.x == 0) fn();
+        __syncthreads();
+    };
+    bool have_amax = false;                     // RANGE_FREE: alpha^max computed once (bitwise the same)
+    auto fin = [&](int stage, int final_check) {
+        finalize_body<F, NDIM, true>(a.partials, np, &sst, g, fp, a.dxd, stage, final_check, nullptr, nullptr, 0,
+                                     have_amax);
+        __syncthreads();
+        if (stage == 0 && !final_check && sst.active) have_amax = true;
+    };
+    for (int k = 1; k < a.ntau; ++k) {
+        ctl([&] { begin_body(&sst, a.tau[k]); });
+        while (sst.active) {
+            const long long s0 = sst.steps;
+            if (a.low) {                          // Alg. 2, Euler (LOW): pass 1, finalize, pass 2
+                pass1_generic_body<NDIM, R, true>(g, buf[cur], a.partials, &sst);
+                grid_barrier(a.bar, gen);
+                fin(0, 0);
+                pass2_generic_body<F, NDIM, R, true>(g, buf[cur], nullptr, a.T, buf[cur ^ 1], &sst, fp, STAGE_EULER, a.brt);
+                grid_barrier(a.bar, gen);
+            } else {                              // TVD-RK2 (MEDIUM): two stages (A10)
+                pass1_generic_body<NDIM, R, true>(g, buf[0], a.partials, &sst);
+                grid_barrier(a.bar, gen);
+                fin(0, 0);
+                pass2_generic_body<F, NDIM, R, true>(g, buf[0], nullptr, a.T, buf[1], &sst, fp, STAGE_RK1, a.brt);
+                grid_barrier(a.bar, gen);
+                pass1_generic_body<NDIM, R, true>(g, buf[1], a.partials, &sst);
+                grid_barrier(a.bar, gen);
+                fin(1, 0);
+                pass2_generic_body<F, NDIM, R, true>(g, buf[1], buf[0], a.T, buf[0], &sst, fp, STAGE_RK2, a.brt);
+                grid_barrier(a.bar, gen);
+            }
+            ctl([&] { advance_body(&sst); });
+            if (a.low && sst.steps != s0) cur ^= 1;
+        }
+        if (sst.status) break;                    // numeric failure: no snapshot, no final guard
+        const float *src = buf[a.low ? cur : 0];
+        float *dst = a.out + (long long)k_out * P;
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (long long)gridDim.x * blockDim.x)
+            dst[i] = __ldcg(src + i);
+        ++k_out;
+    }
+    if (!sst.status) {                            // final guard on the last V (reading A19)
+        ctl([&] { force_active_body(&sst); });
+        pass1_generic_body<NDIM, R, true>(g, buf[a.low ? cur : 0], a.partials, &sst);
+        grid_barrier(a.bar, gen);
+        fin(0, 1);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.st = sst;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -405,6 +540,7 @@ typedef void (*srange_fn)(const float *, int, DevState *, const float *);
 typedef void (*amax3_fn)(GridDev, FParams, const DevState *, float *);
 typedef void (*red_fn)(const float *, int, const DevState *, float *);
 typedef void (*guard_fn)(const float *, int, DevState *, const float *, int);
+typedef void (*res_fn)(GridDev, FParams, ResidentArgs);
 
 struct KernelSet {
     pass1_fn pass1 = nullptr;
@@ -414,6 +550,7 @@ struct KernelSet {
     guard_fn guard = nullptr;
     srange_fn srange = nullptr;   // DEPS3 functors only
     amax3_fn amax3 = nullptr;
+    res_fn res = nullptr;         // k_resident (not for DEPS3 functors: their alpha^max is grid-wide)
     bool range_free = false;
     TiledFns tiled;      // tiled family (may be empty)
     StreamFnsAll stream; // stream family (may be empty)
@@ -432,6 +569,8 @@ static KernelSet make_set() {
     if constexpr (F::DEPS3) {
         k.srange = k_store_range<NDIM>;
         k.amax3 = k_amax3<F, NDIM>;
+    } else {
+        k.res = k_resident<F, NDIM, R>;
     }
     if constexpr (F::SEPARABLE) {      // the tiled / stream families assemble separable Hamiltonians only
         k.tiled = tiled_fns<F, NDIM, R>();
@@ -486,6 +625,9 @@ struct odp_grid {
     odp_loopback *lb = nullptr;   // test transport: slabs of one process on one GPU (odp_grid_partition_loopback)
     float *d_range = nullptr;     // [-minD, maxD, maxabs, nan] of the current stage (allreduced)
     float *d_amax = nullptr;      // per-CTA alpha^max of k_amax3 (DEPS3 functors)
+    double *d_tau = nullptr;      // k_resident: device copy of the save times (capacity tau_cap)
+    int tau_cap = 0;
+    unsigned *d_bar = nullptr;    // k_resident: grid barrier counter
     // device cache (allocated lazily on the device current at the first solve)
     int device = -1;
     float *d_tab = nullptr;
@@ -525,6 +667,8 @@ static void free_device(odp_grid *g) {
     if (g->h_ttr) cudaFreeHost(g->h_ttr);
     cudaFree(g->d_stage);
     g->d_stage = nullptr; g->stage_elems = 0;
+    cudaFree(g->d_tau); cudaFree(g->d_bar);
+    g->d_tau = nullptr; g->tau_cap = 0; g->d_bar = nullptr;
     g->d_ttr = nullptr; g->h_ttr = nullptr;
     if (g->own_stream) cudaStreamDestroy(g->own_stream);
     if (g->side_stream) cudaStreamDestroy(g->side_stream);
@@ -1030,6 +1174,17 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
     if (!use_march && !use_stream && (want_kernel == ODP_KERNEL_AUTO || want_kernel == ODP_KERNEL_TILED) && ks.tiled.pass1)
         use_tiled = tiled_plan(gd, R, nsm, &tp);
     if (want_kernel == ODP_KERNEL_TILED && !use_tiled) return fail(ODP_EINVAL, "tiled kernels do not cover this grid");
+    // resident (one cooperative launch per solve): asked for, or AUTO on a small single-rank grid
+    // without per-launch timing (ODP_RESIDENT_MAX_POINTS, default 2^18 nodes: ~1 MB per array)
+    const long long res_max = getenv("ODP_RESIDENT_MAX_POINTS") ? atoll(getenv("ODP_RESIDENT_MAX_POINTS")) : (1LL << 18);
+    const bool res_ok = ks.res && g->nranks == 1 && !g->comm && !g->lb && !(opts && opts->kernel_ms) &&
+                        !(opts && opts->single_pass);
+    if (want_kernel == ODP_KERNEL_RESIDENT && !res_ok)
+        return fail(ODP_EINVAL, "resident kernel: one rank, no kernel_ms / single_pass, and a dynamics whose alpha^max "
+                                "enumerates <= 2 axes");
+    const bool use_resident = want_kernel == ODP_KERNEL_RESIDENT ||
+                              (want_kernel == ODP_KERNEL_AUTO && res_ok && local_points(g) <= res_max);
+    if (use_resident) use_march = use_stream = use_tiled = false;
     if (use_march) {
         if (march_prepare(mfn, mp, nsm)) return fail(ODP_ECUDA, "march kernel attribute setup failed");
         if ((st = ensure_device(g, mp.grid))) return st;
@@ -1089,6 +1244,43 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
     if (write_initial) {
         CUDA_TRY(cudaMemcpyAsync(out, V0, bytes, cudaMemcpyDeviceToDevice, s));
         k_out = 1;
+    }
+
+    if (use_resident) {
+        int occ = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.res, block, 0));
+        if (occ < 1) return fail(ODP_ECUDA, "k_resident does not fit on an SM");
+        long long nb = std::min<long long>(want_blocks, (long long)occ * nsm);
+        if (getenv("ODP_RESIDENT_CTAS")) nb = std::max(1LL, std::min<long long>(nb, atoll(getenv("ODP_RESIDENT_CTAS"))));
+        if ((st = ensure_device(g, (int)nb))) return st;
+        if (g->tau_cap < ntau) {
+            cudaFree(g->d_tau);
+            g->d_tau = nullptr;
+            g->tau_cap = 0;
+            CUDA_TRY(cudaMalloc(&g->d_tau, (size_t)ntau * sizeof(double)));
+            g->tau_cap = ntau;
+        }
+        if (!g->d_bar) CUDA_TRY(cudaMalloc(&g->d_bar, sizeof(unsigned)));
+        CUDA_TRY(cudaMemcpyAsync(g->d_tau, tau, (size_t)ntau * sizeof(double), cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemsetAsync(g->d_bar, 0, sizeof(unsigned), s));
+        ResidentArgs ra;
+        ra.buf0 = buf[0]; ra.buf1 = buf[1]; ra.T = T; ra.out = out; ra.tau = g->d_tau; ra.ntau = ntau;
+        ra.k_out0 = k_out; ra.partials = g->d_partials; ra.dxd = g->d_dx; ra.st = g->d_state; ra.bar = g->d_bar;
+        ra.low = accuracy == ODP_LOW; ra.brt = brt;
+        void *kargs[] = {&gd, &fp, &ra};
+        CUDA_TRY(cudaLaunchCooperativeKernel((const void *)ks.res, dim3((unsigned)nb), dim3(block), kargs, 0, s));
+        ++g->launches;
+        CUDA_TRY(cudaMemcpyAsync(g->h_state, g->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+        if (odp_status ss = sync_stream(g, s)) return ss;
+        if (opts) {
+            if (opts->tau_reached) *opts->tau_reached = g->h_state->tau;
+            if (opts->steps_taken) *opts->steps_taken = g->h_state->steps;
+            if (opts->stages_taken) *opts->stages_taken = g->h_state->stages;
+            if (opts->single_pass_used) *opts->single_pass_used = 0;
+        }
+        if (g->h_state->status)
+            return fail(ODP_ENUMERIC, "numerical failure (NaN or |V| > 1e10) at tau = %.9g", g->h_state->tau);
+        return ODP_OK;
     }
 
     std::vector<Launch> launches;

@@ -12,7 +12,7 @@ from tests.parity_util import (TOL, assert_parity, assert_parity_envelope, asser
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = ["generic", "tiled", "stream", "march", "auto"]
+KERNELS = ["generic", "tiled", "stream", "march", "resident", "auto"]
 
 SMALL = [
     # (dynamics, params, N, lo, hi, periodic)
