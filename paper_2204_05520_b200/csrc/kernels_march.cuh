@@ -56,6 +56,12 @@ namespace odp {
 #ifndef ODP_MARCH_WAIT
 #define ODP_MARCH_WAIT 1       // 1: mbarrier try_wait with a suspend hint; 0: try_wait + nanosleep back-off
 #endif
+#ifndef ODP_MARCH_WAITP
+#define ODP_MARCH_WAITP 1      // the producer's wait on a released stage (modes of mbar_wait_mode)
+#endif
+#ifndef ODP_MARCH_RELAY
+#define ODP_MARCH_RELAY 0      // 1: one compute warp waits on the copies, named barrier for the rest
+#endif
 #ifndef ODP_MARCH_SLEEP_NS
 #define ODP_MARCH_SLEEP_NS 64   // back-off of the ODP_MARCH_WAIT = 0 wait loop
 #endif
@@ -429,7 +435,32 @@ __device__ __forceinline__ MarchUnit march_unit(const MarchArgs &a, int Nml, int
 
 // mbarrier wait with back-off: a warp that finds its data missing sleeps instead of spinning, so
 // it does not take issue slots from the warps that are computing
+// mode 2: non-blocking test_wait in a tight loop (fastest wake-up, spends issue slots);
+// mode 3: try_wait without a suspend-time hint (the hardware's default time limit) in a loop
+template <int MODE>
+__device__ __forceinline__ void mbar_wait_mode(uint64_t *bar, uint32_t parity) {
+    if constexpr (MODE == 2) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "TW_%=:\n\t"
+            "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra TW_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+    } else if constexpr (MODE == 3) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "TY_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra TY_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+    } else {
+        mbar_wait(bar, parity);
+    }
+}
+
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+#if ODP_MARCH_WAIT == 2 || ODP_MARCH_WAIT == 3
+    mbar_wait_mode<ODP_MARCH_WAIT>(bar, parity);
+    return;
+#endif
 #if ODP_MARCH_WAIT == 1
     mbar_wait(bar, parity);      // try_wait with a suspend-time hint: the hardware parks the warp
     return;
@@ -450,8 +481,11 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) 
     }
 }
 
-template <class F, int NDIM, int R, int NP, bool PASS2, int CN1 = 0, int CB = 0, int NST = 2>
-__global__ void __launch_bounds__(MARCH_MAXT1, ODP_MARCH_MINB1)
+// LBT / LBM: the launch bounds (threads per CTA, CTAs per SM) the register budget is sized for;
+// shape-specialised instances with fewer rows per block may set them to their own block size
+template <class F, int NDIM, int R, int NP, bool PASS2, int CN1 = 0, int CB = 0, int NST = 2,
+          int LBT = MARCH_MAXT1, int LBM = ODP_MARCH_MINB1>
+__global__ void __launch_bounds__(LBT, LBM)
 k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, const float *__restrict__ T,
         float *out, float *partials, const DevState *st, FParams fp, int kind, int brt) {
     static_assert(NP == 1, "the march family computes node pairs (VEC = 2)");
@@ -688,8 +722,11 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
             make_table(U);
             for (int j = U.m0; j < U.m1; ++j, ++sn) {
                 const int sr = sn - NST;                     // the step whose buffers step sn reuses
-                if (sr >= 0) mbar_wait_sleep(&empty[sr % NST], (uint32_t)((sr / NST) & 1));
+                if (sr >= 0) mbar_wait_mode<ODP_MARCH_WAITP>(&empty[sr % NST], (uint32_t)((sr / NST) & 1));
                 issue(U, j, sn, j == U.m0 ? 0 : R);
+#ifdef ODP_MARCH_PDELAY_NS             // experiment: a slower producer (is the copy issue on the critical path?)
+                __nanosleep(ODP_MARCH_PDELAY_NS);
+#endif
             }
             ui = grab();
         }
@@ -781,7 +818,15 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                         vin = ghost2(e, in, (float)(kin - Nm + 1));
                     }
                 }
+#if ODP_MARCH_RELAY
+                // the step's copies landed: compute warp 0 alone waits on the transaction barrier (its
+                // waits wake on every copy's completion), then releases the other compute warps
+                // through a hardware named barrier, where waiting warps take no issue slots
+                if (tid < 32) mbar_wait_sleep(&tmab[st0], (uint32_t)sph);
+                asm volatile("bar.sync 1, %0;" ::"r"(nwc * 32) : "memory");
+#else
                 mbar_wait_sleep(&tmab[st0], (uint32_t)sph);        // the step's copies landed
+#endif
                 const uint32_t rcs = rb_s + (uint32_t)(rs0 * RSZ * 4);      // this thread's nodes in the centre tile
                 const uint32_t sbs = sb_s + (uint32_t)(st0 * NSS * SSZ * 4); // ... in side slot 0
 
@@ -1037,13 +1082,13 @@ struct MarchPlan {
     size_t smem = 0;
 };
 
-template <class F, int NDIM, int R, int CN1, int CB, int NST = 2>
+template <class F, int NDIM, int R, int CN1, int CB, int NST = 2, int LBT = MARCH_MAXT1, int LBM = ODP_MARCH_MINB1>
 void march_add(MarchFnsAll &t) {
     if constexpr (NDIM >= 3) {
         MarchInst &m = t.inst[t.ninst++];
         m.n1 = CN1; m.b = CB; m.nst = NST;
-        m.pass1 = k_march<F, NDIM, R, 1, false, CN1, CB, NST>;
-        m.pass2 = k_march<F, NDIM, R, 1, true, CN1, CB, NST>;
+        m.pass1 = k_march<F, NDIM, R, 1, false, CN1, CB, NST, LBT, LBM>;
+        m.pass2 = k_march<F, NDIM, R, 1, true, CN1, CB, NST, LBT, LBM>;
     }
 }
 
@@ -1055,6 +1100,13 @@ MarchFnsAll march_fns() {
         t.pass2 = k_march<F, NDIM, R, 1, true>;
         if constexpr (std::is_same<F, FDoubleInt6D>::value) {     // c4 (30^6), c5 (64 x 48^5)
             march_add<F, NDIM, R, 30, 30, 2>(t);
+#ifdef ODP_MARCH_EXPERIMENTS       // register budget vs warps per SM (tried and not kept)
+            if constexpr (R == 2) {
+                march_add<F, NDIM, R, 30, 30, 4, 512, 1>(t);     // 1 CTA/SM, no spills, deep pipeline
+                march_add<F, NDIM, R, 30, 10, 3, 192, 4>(t);     // 4 CTAs/SM, 80 registers
+                march_add<F, NDIM, R, 30, 10, 2, 192, 4>(t);
+            }
+#endif
             march_add<F, NDIM, R, 48, 16, 2>(t);
             if constexpr (R == 1) march_add<F, NDIM, R, 48, 16, 4>(t);   // c5 LOW
         } else if constexpr (std::is_same<F, FCar5D>::value && R == 2) {   // c3
@@ -1197,6 +1249,9 @@ inline int march_prepare(const MarchFns &t, MarchPlan &p, int nsm) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, (const void *)t.pass2, p.block, p.smem) != cudaSuccess) return 1;
     const int occ = std::max(1, std::min(occ1, occ2));
     p.grid = std::min(p.a.units, nsm * occ);
+    if (getenv("ODP_MARCH_VERBOSE"))
+        fprintf(stderr, "march plan: B=%d threads=%d smem=%zu occupancy=%d/%d grid=%d units=%d K=%d specialised=%d\n",
+                p.a.B, p.block, p.smem, occ1, occ2, p.grid, p.a.units, p.a.K, t.specialised);
     return 0;
 }
 

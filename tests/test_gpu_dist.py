@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("name,N,acc", [("c4", (12, 10, 12, 10, 12, 10), "medium"), ("c4", (12, 10, 12, 10, 12, 10), "low"),
                                         ("c1", (41, 41, 36), "low"), ("c3", (10, 9, 12, 9, 8), "medium")])
-@pytest.mark.parametrize("kernel", ["auto", "generic"])
+@pytest.mark.parametrize("kernel", ["march", "generic"])   # "auto" is the resident kernel on one rank
 def test_one_rank_communicator_path_is_bitwise(name, N, acc, kernel):
     import torch
     import paper_2204_05520_b200 as odp
@@ -42,8 +42,8 @@ def test_single_pass_is_bitwise_the_two_pass_solve(name, N, acc):
     w = coarsened(CONFIGS[name], N, tau=(0.0, 0.05, 0.1))
     w = w.__class__(**{**w.__dict__, "accuracy": acc, "cfl": 0.8 if acc == "low" else 0.5})
     V0 = torch.from_numpy(make_v0(w, seed=2)).cuda()
-    ref, rinfo = odp.solve_workload(w, V0)
-    out, info = odp.solve_workload(w, V0, single_pass=True)
+    ref, rinfo = odp.solve_workload(w, V0, kernel="march")      # AUTO would run k_resident here
+    out, info = odp.solve_workload(w, V0, kernel="march", single_pass=True)
     assert info["single_pass"] == (name != "c2")      # CAR4D's alpha depends on the range's sign set
     assert info["steps"] == rinfo["steps"] and info["stages"] == rinfo["stages"]
     np.testing.assert_array_equal(out.cpu().numpy(), ref.cpu().numpy())

@@ -21,5 +21,5 @@ for r in r02_c4 r02_c5low; do
   ncu -i gpurun_out/$r.ncu-rep --page source --csv --print-source sass > gpurun_out/${r}_sass.csv 2>/dev/null
 done
 gzip -f gpurun_out/*_sass.csv
-rm -f gpurun_out/r02_c5low.ncu-rep
+rm -f gpurun_out/r02_c5low.ncu-rep gpurun_out/r02_c4.ncu-rep
 ls -la gpurun_out/
