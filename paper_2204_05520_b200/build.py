@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -20,11 +21,26 @@ def sources():
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*")) + [os.path.join(ROOT, "include", "odp.h")])
 
 
+def source_hash(check: bool = False) -> str:
+    """sha256 over the sources, the nvcc flags and the variant: the build is redone when it changes
+    (file contents, not mtimes: a checkout or a copy to the GPU box does not trigger a rebuild)."""
+    h = hashlib.sha256()
+    h.update(" ".join(NVCC_FLAGS + (["-DODP_CHECK"] if check else [])).encode())
+    for p in sources():
+        h.update(os.path.relpath(p, ROOT).encode())
+        with open(p, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
 def needs_build(lib: str = LIB) -> bool:
     if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(lib)
-    return any(os.path.getmtime(p) > t for p in sources())
+    stamp = lib + ".sha256"
+    if not os.path.exists(stamp):
+        return True
+    with open(stamp) as fh:
+        return fh.read().strip() != source_hash(check=lib == LIB_CHECK)
 
 
 def build(force: bool = False, verbose: bool = False, check: bool = False) -> str:
@@ -40,6 +56,8 @@ def build(force: bool = False, verbose: bool = False, check: bool = False) -> st
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
     os.replace(tmp, lib)
+    with open(lib + ".sha256", "w") as fh:
+        fh.write(source_hash(check=check) + "\n")
     return lib
 
 

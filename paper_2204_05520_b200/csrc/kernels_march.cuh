@@ -56,6 +56,12 @@ namespace odp {
 #ifndef ODP_MARCH_WAIT
 #define ODP_MARCH_WAIT 1       // 1: mbarrier try_wait with a suspend hint; 0: try_wait + nanosleep back-off
 #endif
+#ifndef ODP_MARCH_ECOUNT
+#define ODP_MARCH_ECOUNT 0     // 1: stage release through a plain shared counter the producer polls
+#endif
+#ifndef ODP_MARCH_ECOUNT_NS
+#define ODP_MARCH_ECOUNT_NS 32 // the producer's poll back-off (ODP_MARCH_ECOUNT = 1)
+#endif
 #ifndef ODP_MARCH_WAITP
 #define ODP_MARCH_WAITP 1      // the producer's wait on a released stage (modes of mbar_wait_mode)
 #endif
@@ -687,7 +693,11 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     if (tid == 0) {
         for (int b = 0; b < NST; ++b) {
             mbar_init(&tmab[b], 1);
+#if ODP_MARCH_ECOUNT
+            *reinterpret_cast<volatile unsigned int *>(&empty[b]) = 0u;   // plain release counter
+#else
             mbar_init(&empty[b], nwc);
+#endif
             mbar_init(&ubar[b], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -722,7 +732,20 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
             make_table(U);
             for (int j = U.m0; j < U.m1; ++j, ++sn) {
                 const int sr = sn - NST;                     // the step whose buffers step sn reuses
+#if ODP_MARCH_ECOUNT
+                if (sr >= 0) {       // the (sr / NST + 1)-th release of stage sr % NST: nwc arrivals each
+                    const unsigned int want = (unsigned int)(sr / NST + 1) * (unsigned int)nwc;
+                    const uint32_t ea = smem_u32(&empty[sr % NST]);
+                    unsigned int have;
+                    for (;;) {
+                        asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(have) : "r"(ea) : "memory");
+                        if ((int)(have - want) >= 0) break;
+                        __nanosleep(ODP_MARCH_ECOUNT_NS);
+                    }
+                }
+#else
                 if (sr >= 0) mbar_wait_mode<ODP_MARCH_WAITP>(&empty[sr % NST], (uint32_t)((sr / NST) & 1));
+#endif
                 issue(U, j, sn, j == U.m0 ? 0 : R);
 #ifdef ODP_MARCH_PDELAY_NS             // experiment: a slower producer (is the copy issue on the critical path?)
                 __nanosleep(ODP_MARCH_PDELAY_NS);
@@ -1032,7 +1055,14 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                     for (int k = 0; k < R; ++k) win[k] = win[k + 1];
                 }
                 __syncwarp();
+#if ODP_MARCH_ECOUNT
+                // this warp is done with the step's buffers: a plain shared-memory release counter (an
+                // mbarrier arrive would wake every warp sleeping on the copy barriers, 15 times a step)
+                if ((tid & 31) == 0)
+                    asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(smem_u32(&empty[st0])) : "memory");
+#else
                 if ((tid & 31) == 0) mbar_arrive(&empty[st0]);   // this warp is done with the step's buffers
+#endif
                 if (++rs0 == RS) rs0 = 0;
                 if (++rsw == RS) rsw = 0;
                 if (++st0 == NST) { st0 = 0; sph ^= 1; }
@@ -1208,7 +1238,7 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     for (int o = 0; o < 3; ++o) a.sn[o] = o < MA ? g.N[o] : 1;
     a.b1 = 1;
     if (MA == 3) {
-        int want = 6;
+        int want = 3;                               // c4 sweep (ODP_MARCH_B1 = 1..30): 3 best, +1.7 % over 6
         if (const char *env = getenv("ODP_MARCH_B1")) want = std::max(1, atoi(env));
         for (int b = std::min(want, g.N[1]); b >= 1; --b)
             if (g.N[1] % b == 0) { a.b1 = b; break; }

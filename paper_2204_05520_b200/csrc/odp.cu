@@ -22,10 +22,21 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX: ranges are free unless a profiler injects itself
+
 #include "../../include/odp.h"
 #include "kernels_march.cuh"
 #include "kernels_ttr.cuh"
 #include "kernels_vi.cuh"
+
+// NVTX ranges around the host orchestration (SURVEY.md §5 tracing): solve, save interval, halo
+// exchange, range allreduce, resident launch -- visible in Nsight Systems / ncu --nvtx filters
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 using namespace odp;
 
@@ -1039,6 +1050,7 @@ static odp_status lb_range_allreduce(odp_grid *g, int n, cudaStream_t s) {
 // low halo.  Slabs are contiguous row-major ranges, so every message is one contiguous range.
 static odp_status halo_exchange(odp_grid *g, float *W, int R, cudaStream_t s) {
     if (g->nranks <= 1) return ODP_OK;
+    NvtxRange nv("odp halo_exchange");
     if (g->lb) return lb_halo_exchange(g, W, R, s);
     nccl::Api &a = nccl::api();
     const size_t plane = (size_t)plane_of(g), cnt = (size_t)R * plane;
@@ -1057,6 +1069,7 @@ static odp_status halo_exchange(odp_grid *g, float *W, int R, cudaStream_t s) {
 
 // allreduce(max) of the stage's range record [-minD, maxD, maxabs, nan] over the ranks
 static odp_status range_allreduce(odp_grid *g, int n, cudaStream_t s) {
+    NvtxRange nv("odp range_allreduce");
     if (g->lb) return lb_range_allreduce(g, n, s);
     if (!g->comm) return ODP_OK;
     NCCL_TRY(nccl::api().AllReduce(g->d_range, g->d_range, (size_t)(2 * n + 2), nccl::Float32, nccl::Max, g->comm, s));
@@ -1268,6 +1281,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
         ra.k_out0 = k_out; ra.partials = g->d_partials; ra.dxd = g->d_dx; ra.st = g->d_state; ra.bar = g->d_bar;
         ra.low = accuracy == ODP_LOW; ra.brt = brt;
         void *kargs[] = {&gd, &fp, &ra};
+        NvtxRange nv("odp k_resident (whole solve)");
         CUDA_TRY(cudaLaunchCooperativeKernel((const void *)ks.res, dim3((unsigned)nb), dim3(block), kargs, 0, s));
         ++g->launches;
         CUDA_TRY(cudaMemcpyAsync(g->h_state, g->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s));
@@ -1445,6 +1459,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
     };
     struct GraphGuard { std::function<void()> f; ~GraphGuard() { f(); } } graph_guard{free_graphs};
     for (int k = 1; k < ntau && rs == ODP_OK; ++k) {
+        NvtxRange nv("odp save interval");
         k_begin<<<1, 1, 0, s>>>(g->d_state, tau[k]);
         ++g->launches;
         CUDA_TRY(cudaMemcpyAsync(g->h_state, g->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s));
@@ -1533,6 +1548,7 @@ extern "C" odp_status odp_hj_solve(odp_grid *g, int dynamics_id, const double *p
                                    const double *tau, int ntau, int accuracy, int mode, float *out,
                                    const odp_solve_opts *opts) {
     g_err.clear();
+    NvtxRange nv("odp_hj_solve");
     return solve_device(g, dynamics_id, params, nparams, V0, tau, ntau, accuracy, mode, out, opts);
 }
 
@@ -1540,6 +1556,7 @@ extern "C" odp_status odp_hj_solve_host(odp_grid *g, int dynamics_id, const doub
                                         const float *V0, const double *tau, int ntau, int accuracy, int mode,
                                         float *out, const odp_solve_opts *opts) {
     g_err.clear();
+    NvtxRange nv("odp_hj_solve_host");
     odp_status st = validate(g, dynamics_id, params, nparams, tau, ntau, accuracy, mode);
     if (st) return st;
     if (!V0 || !out) return fail(ODP_EINVAL, "NULL V0/out");
@@ -1782,6 +1799,7 @@ static odp_status ttr_device(odp_grid *g, int dyn, const double *params, int npa
 extern "C" odp_status odp_ttr_solve(odp_grid *g, int dynamics_id, const double *params, int nparams,
                                     const float *V0, float *phi, const odp_ttr_opts *opts) {
     g_err.clear();
+    NvtxRange nv("odp_ttr_solve");
     return ttr_device(g, dynamics_id, params, nparams, V0, phi, opts);
 }
 
@@ -1898,6 +1916,7 @@ static odp_status vi_device(odp_grid *g, int model, const double *params, int np
 extern "C" odp_status odp_vi_solve(odp_grid *g, int model_id, const double *params, int nparams, const float *R,
                                    float *V, const odp_vi_opts *opts) {
     g_err.clear();
+    NvtxRange nv("odp_vi_solve");
     return vi_device(g, model_id, params, nparams, R, V, opts);
 }
 

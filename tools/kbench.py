@@ -16,11 +16,11 @@ w = w.__class__(**{**w.__dict__, "tau": (0.0, t1)})
 V0 = torch.from_numpy(make_v0(w)).cuda()
 g = odp.Grid(w.N, w.lo, w.hi, w.periodic_mask)
 out = torch.empty((1,) + w.N, device="cuda")
-odp.hj_solve(g, w.dynamics, w.params, V0, w.tau, w.accuracy, w.mode, out=out, cfl=w.cfl, kernel=kernel)
+odp.hj_solve(g, w.dynamics, w.params, V0, w.tau, w.accuracy, w.mode, out=out, cfl=w.cfl, kernel=kernel, raise_on_error=False)
 best = None
 for _ in range(3):
     _, info = odp.hj_solve(g, w.dynamics, w.params, V0, w.tau, w.accuracy, w.mode, out=out, cfl=w.cfl, kernel=kernel,
-                           timing=True)
+                           timing=True, raise_on_error=False)
     k = info["kernel_ms"]
     st = info["stages"]
     cur = (k["pass1"] / st, k["pass2"] / st)
