@@ -56,6 +56,9 @@ namespace odp {
 #ifndef ODP_MARCH_WAIT
 #define ODP_MARCH_WAIT 1       // 1: mbarrier try_wait with a suspend hint; 0: try_wait + nanosleep back-off
 #endif
+#ifndef ODP_MARCH_LEANP
+#define ODP_MARCH_LEANP 1      // producer: per-unit copy descriptors in registers (0: round-1 issue())
+#endif
 #ifndef ODP_MARCH_ECOUNT
 #define ODP_MARCH_ECOUNT 0     // 1: stage release through a plain shared counter the producer polls
 #endif
@@ -730,6 +733,31 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
         while (ui >= 0) {
             const MarchUnit U = march_unit<MA>(a, Nml, mlo, ui);
             make_table(U);
+#if ODP_MARCH_LEANP
+            // this lane's copy descriptor for the whole unit: only the marching offset, the stage and
+            // the ring slot change from step to step (round 1's issue() re-derived everything from
+            // the shared table every step, ~90 instructions + a REDUX on the producer's serial path)
+            const long long colb = U.cbase - (long long)mlo * M;   // element offset of global marching index 0
+            uint32_t d_nb = 0, d_w0 = 0, d_w1 = 0, d_dst = 0, d_d0 = 0, d_d1 = 0;
+            long long d_src = 0, d_s0 = 0;
+            if (lane < NSS) {
+                d_nb = t_snb[lane];
+                d_src = colb + t_soff[lane];
+                d_dst = smem_u32(side + lane * SSZ + MARCH_SMARG);
+            } else if (lane - NSS <= R) {
+                d_nb = (uint32_t)t_ring[1];
+                d_src = colb + t_ring[0];
+                d_dst = smem_u32(ring + t_ring[2]);
+                d_w0 = (uint32_t)t_ring[3];
+                d_w1 = (uint32_t)t_ring[4];
+                d_s0 = colb + t_ring[6];
+                d_d0 = smem_u32(ring + RMG);
+                d_d1 = smem_u32(ring + t_ring[5]);
+            }
+            if (a.dbg & 4) d_nb = d_w0 = d_w1 = 0;      // experiment: no data movement (garbage tiles)
+            const uint32_t side_bytes = __reduce_add_sync(0xffffffffu, lane < NSS ? d_nb : 0u);
+            const uint32_t ring_bytes = (a.dbg & 4) ? 0u : (uint32_t)(t_ring[1] + t_ring[3] + t_ring[4]);
+#endif
             for (int j = U.m0; j < U.m1; ++j, ++sn) {
                 const int sr = sn - NST;                     // the step whose buffers step sn reuses
 #if ODP_MARCH_ECOUNT
@@ -746,7 +774,52 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
 #else
                 if (sr >= 0) mbar_wait_mode<ODP_MARCH_WAITP>(&empty[sr % NST], (uint32_t)((sr / NST) & 1));
 #endif
+#if ODP_MARCH_LEANP
+                {
+                    const int stg = sn % NST;
+                    uint64_t *bar = &tmab[stg];
+                    const int kb = j == U.m0 ? 0 : R;           // ring tiles j + kb .. j + klast
+                    const int klast = min(R, U.m1 - 1 - j);
+                    const uint32_t nring = klast >= kb ? (uint32_t)(klast - kb + 1) : 0u;
+                    if (lane == 0) mbar_expect_tx(bar, side_bytes + nring * ring_bytes);
+                    __syncwarp();
+                    uint32_t n = 0, n0 = 0, n1 = 0, dd = 0, off = 0;
+                    long long se = 0, mo = 0;
+                    if (lane < NSS) {
+                        n = d_nb;
+                        dd = d_dst + (uint32_t)(stg * NSS * SSZ * 4);
+                        se = d_src + (long long)j * M;
+                    } else {
+                        const int k = lane - NSS;
+                        if (k >= kb && k <= klast) {
+                            off = (uint32_t)(((sn + k) % RS) * RSZ * 4);
+                            mo = (long long)(j + k) * M;
+                            n = d_nb; n0 = d_w0; n1 = d_w1;
+                            dd = d_dst + off;
+                            se = d_src + mo;
+                        }
+                    }
+#ifdef ODP_CHECK
+                    {
+                        const long long wlo = -2LL * g.stride[0], whi = g.P + 2LL * g.stride[0];
+                        auto chk_copy = [&](uint32_t d, long long e, uint32_t nbytes, int code) {
+                            if (!nbytes) return;
+                            ODP_CHK(e >= wlo && e + nbytes / 4 <= whi, code, e, nbytes);
+                            ODP_CHK(((uintptr_t)(W + e) & 15) == 0 && (d & 15) == 0 && (nbytes & 15) == 0, code + 1, e, nbytes);
+                            odp_chk_smem(d, nbytes, code + 2);
+                        };
+                        chk_copy(dd, se, n, 10);
+                        chk_copy(d_d0 + off, d_s0 + mo, n0, 20);
+                        chk_copy(d_d1 + off, colb + mo, n1, 30);
+                    }
+#endif
+                    if (n) tma_bulk_g2s_u32(dd, W + se, n, bar);
+                    if (n0) tma_bulk_g2s_u32(d_d0 + off, W + d_s0 + mo, n0, bar);
+                    if (n1) tma_bulk_g2s_u32(d_d1 + off, W + colb + mo, n1, bar);
+                }
+#else
                 issue(U, j, sn, j == U.m0 ? 0 : R);
+#endif
 #ifdef ODP_MARCH_PDELAY_NS             // experiment: a slower producer (is the copy issue on the critical path?)
                 __nanosleep(ODP_MARCH_PDELAY_NS);
 #endif
