@@ -344,12 +344,12 @@ __device__ __forceinline__ float abs_k(const FPairDubins3D &, int) { return 0.f;
 struct MarchArgs {
     int M, N2, N1;        // tile size and in-plane extents
     int per2, per1;
-    int QR;               // threads per row = N1 / VEC
+    int xs;               // pass 2's streamed operands staged by TMA: bit 0 the target T, bit 1 Vn
     int B, nrb;           // rows per row block, row blocks per tile
     int nthr;             // B * QR
     int RSZ, SSZ;         // floats per ring / side slot
-    int RGT;              // float offset of the column-ghost table in a ring slot
-    int NSS;              // side slots per buffer (2R per side axis)
+    int xoff;             // float offset of the T / Vn slots ([NST][xn] x SSZ)
+    int xn;               // T / Vn slots per stage (0..2)
     int rmarg;            // leading margin of a ring slot (keeps TMA destinations 16-B aligned)
     int side_off;         // float offset of the side buffers
     int bar_off;          // float offset of the mbarriers
@@ -513,10 +513,13 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     constexpr int RS = R + NST;      // ring slots
     constexpr bool CT = CN1 > 0;     // shape-specialised instance: geometry known at compile time
     constexpr int NSS = 2 * R * MA;  // side slots per stage
+    // pass 2's T / Vn staged by TMA (a.xs): LOW instances only -- in the MEDIUM pass 2 the extra
+    // live state costs spills and occupancy (c4 / c3 / c5-MEDIUM measured slower)
+    constexpr bool XSC = PASS2 && R == 1;
+    const int xs = XSC ? a.xs : 0;
     extern __shared__ __align__(128) float smem[];
     const int N1 = CT ? CN1 : a.N1;
     const int RSZ = CT ? geo_rsz(R, CN1, CB) : a.RSZ;
-    const int RGT = CT ? geo_rgt(R, CN1, CB) : a.RGT;
     const int SSZ = CT ? geo_ssz(CN1, CB) : a.SSZ;
     const int RMG = CT ? geo_rmarg(R, CN1) : a.rmarg;
     float *ring = smem;
@@ -601,7 +604,8 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                 if (per) jo = jo < 0 ? jo + no : jo - no;
                 else ok = false;
             }
-            if (!PASS2 && R == 2 && !face && k == -2) ok = false;     // pass 1 interior: edge i+1/2 only
+            // pass 1 interior: edge i+1/2 only -- the -R tile (ENO2) / the -1 tile (upwind) is never read
+            if (!PASS2 && !face && k == -R) ok = false;
             t_soff[lane] = (long long)(jo - io) * so + (long long)U.r0 * N1;
             t_snb[lane] = ok ? (uint32_t)U.nrow * N1 * 4 : 0u;
         }
@@ -740,6 +744,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
             const long long colb = U.cbase - (long long)mlo * M;   // element offset of global marching index 0
             uint32_t d_nb = 0, d_w0 = 0, d_w1 = 0, d_dst = 0, d_d0 = 0, d_d1 = 0;
             long long d_src = 0, d_s0 = 0;
+            const float *d_base = W;                        // source array of this lane's copy
             if (lane < NSS) {
                 d_nb = t_snb[lane];
                 d_src = colb + t_soff[lane];
@@ -753,9 +758,19 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                 d_s0 = colb + t_ring[6];
                 d_d0 = smem_u32(ring + RMG);
                 d_d1 = smem_u32(ring + t_ring[5]);
+            } else if (XSC && lane - NSS - R - 1 < 2) {
+                // pass 2's streamed operands: lane NSS+R+1 the target T, lane NSS+R+2 Vn (row block of
+                // the step's tile, same element offsets as the centre tile)
+                const int xl = lane - NSS - R - 1;
+                if ((xs >> xl) & 1) {
+                    d_nb = (uint32_t)U.nrow * N1 * 4;
+                    d_src = colb + (long long)U.r0 * N1;
+                    d_base = xl == 0 ? T : Vn;
+                    d_dst = smem_u32(smem + a.xoff + (xl == 1 && (xs & 1) ? SSZ : 0) + MARCH_SMARG);
+                }
             }
             if (a.dbg & 4) d_nb = d_w0 = d_w1 = 0;      // experiment: no data movement (garbage tiles)
-            const uint32_t side_bytes = __reduce_add_sync(0xffffffffu, lane < NSS ? d_nb : 0u);
+            const uint32_t side_bytes = __reduce_add_sync(0xffffffffu, (lane < NSS || (XSC && lane > NSS + R)) ? d_nb : 0u);
             const uint32_t ring_bytes = (a.dbg & 4) ? 0u : (uint32_t)(t_ring[1] + t_ring[3] + t_ring[4]);
 #endif
             for (int j = U.m0; j < U.m1; ++j, ++sn) {
@@ -789,6 +804,10 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                         n = d_nb;
                         dd = d_dst + (uint32_t)(stg * NSS * SSZ * 4);
                         se = d_src + (long long)j * M;
+                    } else if (XSC && lane > NSS + R) {       // T / Vn (pass 2, LOW)
+                        n = d_nb;
+                        dd = d_dst + (uint32_t)(stg * a.xn * SSZ * 4);
+                        se = d_src + (long long)j * M;
                     } else {
                         const int k = lane - NSS;
                         if (k >= kb && k <= klast) {
@@ -808,12 +827,20 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                             ODP_CHK(((uintptr_t)(W + e) & 15) == 0 && (d & 15) == 0 && (nbytes & 15) == 0, code + 1, e, nbytes);
                             odp_chk_smem(d, nbytes, code + 2);
                         };
-                        chk_copy(dd, se, n, 10);
+                        if (XSC && lane > NSS + R) {          // T / Vn: the local slab [0, P)
+                            if (n) {
+                                ODP_CHK(se >= 0 && se + n / 4 <= g.P, 50, se, n);
+                                ODP_CHK(((uintptr_t)(d_base + se) & 15) == 0 && (dd & 15) == 0 && (n & 15) == 0, 51, se, n);
+                                odp_chk_smem(dd, n, 52);
+                            }
+                        } else {
+                            chk_copy(dd, se, n, 10);
+                        }
                         chk_copy(d_d0 + off, d_s0 + mo, n0, 20);
                         chk_copy(d_d1 + off, colb + mo, n1, 30);
                     }
 #endif
-                    if (n) tma_bulk_g2s_u32(dd, W + se, n, bar);
+                    if (n) tma_bulk_g2s_u32(dd, (XSC ? d_base : W) + se, n, bar);
                     if (n0) tma_bulk_g2s_u32(d_d0 + off, W + d_s0 + mo, n0, bar);
                     if (n1) tma_bulk_g2s_u32(d_d1 + off, W + colb + mo, n1, bar);
                 }
@@ -833,6 +860,8 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
         int st0 = 0, sph = 0;                            // it % NST (stage), (it / NST) & 1
         const uint32_t rb_s = smem_u32(ring + toff);    // this thread's nodes in ring slot 0 (bytes)
         const uint32_t sb_s = smem_u32(side + sloc);    // ... in side slot 0 of stage 0
+        const uint32_t xb_s = smem_u32(smem + a.xoff + sloc);   // ... in the T / Vn slots of stage 0 (pass 2)
+        const uint32_t xvo = (xs & 1) ? (uint32_t)SSZ * 4u : 0u;  // Vn's slot after T's
         const uint32_t lof = 4u * (uint32_t)loff, rof = 4u * (uint32_t)roff;
         int rsw = R;                                     // (it + R) % RS: ring slot of the entering window tile
         for (int k = 0;; ++k) {
@@ -888,12 +917,12 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                 }
             }
             float2 vnv = f2s(0.f), ttv = f2s(0.f);         // Vn / target of the current step (pass 2), loaded a step ahead
-            if constexpr (PASS2) {
+            if constexpr (PASS2) {                         // (unless staged by TMA with the step's tiles: xs)
                 if (act) {
                     const long long gi0 = U.cbase + (long long)(m0 - mlo) * M + grow * N1 + qc0;
                     ODP_CHK(gi0 >= 0 && gi0 + 2 <= g.P, 41, gi0, g.P);
-                    if (kind == STAGE_RK2) vnv = *reinterpret_cast<const float2 *>(Vn + gi0);
-                    if (brt && kind != STAGE_RK1) ttv = __ldg(reinterpret_cast<const float2 *>(T + gi0));
+                    if (kind == STAGE_RK2 && !(xs & 2)) vnv = *reinterpret_cast<const float2 *>(Vn + gi0);
+                    if (brt && kind != STAGE_RK1 && !(xs & 1)) ttv = __ldg(reinterpret_cast<const float2 *>(T + gi0));
                 }
             }
 
@@ -1110,6 +1139,11 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                             for (int d = 0; d < NDIM; ++d) { p0[d] = pv[d].x; p1[d] = pv[d].y; }
                             acc = f2(f.ham(a0, p0), f.ham(a1, p1));
                         }
+                        if (xs) {                            // staged operands of this step
+                            const uint32_t xs0 = xb_s + (uint32_t)(st0 * a.xn * SSZ * 4);
+                            if (xs & 1) ttv = lds2(xs0);
+                            if (xs & 2) vnv = lds2(xs0 + xvo);
+                        }
                         const float2 L = add2(ham_fin2(f, acc), dis);
                         float2 v = fma2(f2s(dt), L, v0);                        // W + dt L
                         if (kind == STAGE_RK2) v = mul2(f2s(0.5f), add2(vnv, v));  // (Vn + V2)/2 (A10)
@@ -1118,8 +1152,8 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                         *reinterpret_cast<float2 *>(out + gi) = v;
                         mabs = max3nan(mabs, fabsf(v.x), fabsf(v.y));   // output guard (single-pass solves)
                         if (jg + 1 < m1) {                    // the next step's Vn / target
-                            if (kind == STAGE_RK2) vnv = *reinterpret_cast<const float2 *>(Vn + gi + M);
-                            if (brt && kind != STAGE_RK1) ttv = __ldg(reinterpret_cast<const float2 *>(T + gi + M));
+                            if (kind == STAGE_RK2 && !(xs & 2)) vnv = *reinterpret_cast<const float2 *>(Vn + gi + M);
+                            if (brt && kind != STAGE_RK1 && !(xs & 1)) ttv = __ldg(reinterpret_cast<const float2 *>(T + gi + M));
                         }
                     } else {
                         mabs = max3nan(mabs, fabsf(v0.x), fabsf(v0.y));
@@ -1183,6 +1217,8 @@ struct MarchPlan {
     MarchArgs a;
     int block = 0, grid = 0;
     size_t smem = 0;
+    bool t_ok = false;    // the target is 16-B aligned (TMA source)
+    size_t smem_noxs = 0; // dynamic shared memory without the T / Vn staging slots
 };
 
 template <class F, int NDIM, int R, int CN1, int CB, int NST = 2, int LBT = MARCH_MAXT1, int LBM = ODP_MARCH_MINB1>
@@ -1291,14 +1327,11 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     MarchArgs &a = p->a;
     a.M = (int)M; a.N2 = N2; a.N1 = N1;
     a.per2 = g.per[g.n - 2]; a.per1 = g.per[g.n - 1];
-    a.QR = QR;
     a.B = best;
     a.nrb = (N2 + best - 1) / best;
     a.nthr = best * QR;
     a.RSZ = geo_rsz(R, N1, best);
-    a.RGT = geo_rgt(R, N1, best);
     a.SSZ = geo_ssz(N1, best);
-    a.NSS = NSS;
     a.rmarg = geo_rmarg(R, N1);
     a.side_off = geo_side_off(R, N1, best, nst);
     a.bar_off = geo_bar_off(R, N1, best, NSS, nst);
@@ -1338,18 +1371,45 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     p->block = ((a.nthr + 31) / 32) * 32 + 32;      // compute warps + the producer warp
     p->smem = (size_t)(a.aux_off + 96 + 3 * a.mtab_n) * 4;
     p->smem = std::max(p->smem, (size_t)geo_smem_bytes(R, N1, best, NSS, nst));
+    // pass 2's streamed operands (target T, Vn of RK stage 2) staged by TMA with the step's tiles:
+    // as many slots per stage (0..2) as the shared memory of the chosen occupancy leaves room for
+    // (ODP_MARCH_XS = 0 keeps them as per-thread global loads one step ahead, the round-1 path)
+    a.xs = 0;
+    p->smem_noxs = p->smem;
+    a.xoff = (int)((p->smem / 4 + 31) / 32 * 32);   // 128-B aligned
+    a.xn = 0;
+    {
+        // (march_prepare drops the slots again if, with the static shared memory, they cost a CTA/SM)
+        const size_t cap = (!one_cta && geo_smem_bytes(R, N1, best, NSS, nst) <= 113 * 1024) ? 113 * 1024 : 226 * 1024;
+        int want = ODP_MARCH_LEANP ? 2 : 0;
+        if (const char *env = getenv("ODP_MARCH_XS")) want = std::min(want, std::max(0, atoi(env)));
+        if (R != 1) want = 0;
+        for (int xn = want; xn >= 1; --xn)
+            if ((size_t)(a.xoff + xn * nst * a.SSZ) * 4 <= cap) { a.xn = xn; break; }
+        if (a.xn) p->smem = (size_t)(a.xoff + a.xn * nst * a.SSZ) * 4;
+    }
+    p->t_ok = T && ((uintptr_t)T % 16) == 0;
     p->grid = 0;
     return true;
 }
 
 inline int march_prepare(const MarchFns &t, MarchPlan &p, int nsm) {
-    for (march_fn fn : {t.pass1, t.pass2}) {
-        if (cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) != cudaSuccess)
-            return 1;
-    }
     int occ1 = 0, occ2 = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, (const void *)t.pass1, p.block, p.smem) != cudaSuccess) return 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, (const void *)t.pass2, p.block, p.smem) != cudaSuccess) return 1;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        for (march_fn fn : {t.pass1, t.pass2}) {
+            if (cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) != cudaSuccess)
+                return 1;
+        }
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, (const void *)t.pass1, p.block, p.smem) != cudaSuccess) return 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, (const void *)t.pass2, p.block, p.smem) != cudaSuccess) return 1;
+        // the T / Vn staging slots must not cost a CTA per SM (static shared memory counts too)
+        if (p.a.xn == 0 || p.smem_noxs == p.smem) break;
+        int occ0 = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, (const void *)t.pass2, p.block, p.smem_noxs) != cudaSuccess) return 1;
+        if (occ0 <= std::min(occ1, occ2)) break;
+        p.a.xn = 0;
+        p.smem = p.smem_noxs;
+    }
     const int occ = std::max(1, std::min(occ1, occ2));
     p.grid = std::min(p.a.units, nsm * occ);
     if (getenv("ODP_MARCH_VERBOSE"))
@@ -1370,6 +1430,12 @@ inline void march_pass2(const MarchFns &t, const MarchPlan &p, const GridDev &g,
                         cudaStream_t s, float *guard_partials = nullptr) {
     MarchArgs a = p.a;
     a.wslot = 1;
+    // stage T (and Vn) by TMA where the plan left slots: T first (BRT), then Vn (RK stage 2)
+    const int need = ((brt && kind != STAGE_RK1 && p.t_ok) ? 1 : 0) |
+                     ((kind == STAGE_RK2 && ((uintptr_t)Vn % 16) == 0) ? 2 : 0);
+    a.xs = 0;
+    if (a.xn >= 2) a.xs = need;
+    else if (a.xn == 1) a.xs = (need & 1) ? 1 : need;
     t.pass2<<<p.grid, p.block, p.smem, s>>>(a, g, W, Vn, T, out, guard_partials, st, fp, kind, brt);
 }
 
