@@ -77,6 +77,11 @@ namespace odp {
 #ifndef ODP_MARCH_SELP
 #define ODP_MARCH_SELP 0       // 1: ENO pick as FSET + 3 FMA-pipe ops instead of FSETP + FSEL
 #endif
+#ifdef ODP_MARCH_EXPERIMENTS
+constexpr bool MARCH_EXP = true;   // timing experiments (ODP_MARCH_DBG): the kernels read MarchArgs::dbg
+#else
+constexpr bool MARCH_EXP = false;  // production: dbg is a compile-time 0
+#endif
 constexpr int MARCH_MAXT1 = 512;   // threads per CTA, NP = 1 (compute warps + the producer warp)
 constexpr int MARCH_MAXT2 = 640;   // threads per CTA, NP = 2
 
@@ -517,6 +522,9 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     // live state costs spills and occupancy (c4 / c3 / c5-MEDIUM measured slower)
     constexpr bool XSC = PASS2 && R == 1;
     const int xs = XSC ? a.xs : 0;
+    const int dbg = MARCH_EXP ? a.dbg : 0;
+    // LOW (R = 1) is always forward Euler (odp.cu's step sequence); MEDIUM runs RK stages 1 and 2
+    if constexpr (R == 1) kind = STAGE_EULER;
     extern __shared__ __align__(128) float smem[];
     const int N1 = CT ? CN1 : a.N1;
     const int RSZ = CT ? geo_rsz(R, CN1, CB) : a.RSZ;
@@ -651,7 +659,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                 nbw1 = (uint32_t)t_ring[4];
             }
         }
-        if (a.dbg & 4) nb = nbw0 = nbw1 = 0;          // experiment: no data movement (garbage tiles)
+        if (dbg & 4) nb = nbw0 = nbw1 = 0;          // experiment: no data movement (garbage tiles)
 #ifdef ODP_CHECK
         {
             const long long wlo = -2LL * g.stride[0], whi = g.P + 2LL * g.stride[0];   // W: local planes + 2 halo planes
@@ -689,7 +697,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
             }
     }
     auto load_march = [&](Pt &q, int jg) {            // coordinates of the marching axis at global index jg
-        if (a.mtab_n) {
+        if (CT || a.mtab_n) {                        // (shape-specialised instances always stage it)
             if ((F::NEED_X >> MA) & 1) q.x[MA] = mtab[jg];
             if ((F::NEED_TRIG >> MA) & 1) { q.c[MA] = mtab[a.mtab_n + jg]; q.s[MA] = mtab[2 * a.mtab_n + jg]; }
         } else {
@@ -769,9 +777,9 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                     d_dst = smem_u32(smem + a.xoff + (xl == 1 && (xs & 1) ? SSZ : 0) + MARCH_SMARG);
                 }
             }
-            if (a.dbg & 4) d_nb = d_w0 = d_w1 = 0;      // experiment: no data movement (garbage tiles)
+            if (dbg & 4) d_nb = d_w0 = d_w1 = 0;      // experiment: no data movement (garbage tiles)
             const uint32_t side_bytes = __reduce_add_sync(0xffffffffu, (lane < NSS || (XSC && lane > NSS + R)) ? d_nb : 0u);
-            const uint32_t ring_bytes = (a.dbg & 4) ? 0u : (uint32_t)(t_ring[1] + t_ring[3] + t_ring[4]);
+            const uint32_t ring_bytes = (dbg & 4) ? 0u : (uint32_t)(t_ring[1] + t_ring[3] + t_ring[4]);
 #endif
             for (int j = U.m0; j < U.m1; ++j, ++sn) {
                 const int sr = sn - NST;                     // the step whose buffers step sn reuses
@@ -955,7 +963,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                 const uint32_t rcs = rb_s + (uint32_t)(rs0 * RSZ * 4);      // this thread's nodes in the centre tile
                 const uint32_t sbs = sb_s + (uint32_t)(st0 * NSS * SSZ * 4); // ... in side slot 0
 
-                if (act && !(a.dbg & 2)) {
+                if (act && !(dbg & 2)) {
                     if (in_ring) vin = lds2(rb_s + (uint32_t)(rsw * RSZ * 4));
                     win[R] = vin;
                     const float2 v0 = win[0];
@@ -1299,10 +1307,12 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
         if (b_env >= 1 && b_env <= N2 && b_env * QR + 32 <= MARCH_MAXT1 && (b_env == N2 || (b_env * N1) % 4 == 0)) bb = b_env;
         return bb;
     };
+    // shape-specialised instances read the marching coordinate table from shared memory only
+    const bool mtab_ok = g.N[g.n - 3] <= 1024 && (g.n - 3 != 0 || g.Ng0 <= 1024);
     auto has_inst = [&](int B, int nst) {
         if (generic_only) return nst == 2;
         for (int i = 0; i < all.ninst; ++i)
-            if (all.inst[i].n1 == N1 && all.inst[i].b == B && all.inst[i].nst == nst) return true;
+            if (all.inst[i].n1 == N1 && all.inst[i].b == B && all.inst[i].nst == nst) return mtab_ok;
         return nst == 2;
     };
     int best = 0, nst = 2;
@@ -1318,7 +1328,7 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     fns->pass1 = all.pass1;
     fns->pass2 = all.pass2;
     fns->specialised = 0;
-    for (int i = 0; i < all.ninst && !generic_only; ++i)
+    for (int i = 0; i < all.ninst && !generic_only && mtab_ok; ++i)
         if (all.inst[i].n1 == N1 && all.inst[i].b == best && all.inst[i].nst == nst) {
             fns->pass1 = all.inst[i].pass1;
             fns->pass2 = all.inst[i].pass2;
@@ -1355,7 +1365,9 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
     const long long cols_rb = ncols * a.nrb;
     a.ncols = (int)std::min<long long>(ncols, 1LL << 30);
     a.K = Nm;
-    if (cols_rb < 148LL * 4) a.K = std::max(4, Nm / (int)std::max<long long>(1, (148 * 8) / cols_rb));
+    // few columns: split the marching axis into segments, ~6 units per SM (c2 sweep of ODP_MARCH_K:
+    // 20 best, 1.43e11 vs 1.36e11 at the ~8 per SM segment length 15 and 1.20e11 unsegmented)
+    if (cols_rb < 148LL * 4) a.K = std::max(4, Nm / (int)std::max<long long>(1, (148 * 6) / cols_rb));
 
     if (const char *env = getenv("ODP_MARCH_K")) a.K = std::max(1, atoi(env));
     a.K = std::min(a.K, Nm);
