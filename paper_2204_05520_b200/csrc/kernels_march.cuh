@@ -74,6 +74,9 @@ namespace odp {
 #ifndef ODP_MARCH_SLEEP_NS
 #define ODP_MARCH_SLEEP_NS 64   // back-off of the ODP_MARCH_WAIT = 0 wait loop
 #endif
+#ifndef ODP_MARCH_UNROLL
+#define ODP_MARCH_UNROLL 1     // experiment: unroll the marching loop (window shifts become renames)
+#endif
 #ifndef ODP_MARCH_SELP
 #define ODP_MARCH_SELP 0       // 1: ENO pick as FSET + 3 FMA-pipe ops instead of FSETP + FSEL
 #endif
@@ -524,7 +527,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     const int xs = XSC ? a.xs : 0;
     const int dbg = MARCH_EXP ? a.dbg : 0;
     // LOW (R = 1) is always forward Euler (odp.cu's step sequence); MEDIUM runs RK stages 1 and 2
-    if constexpr (R == 1) kind = STAGE_EULER;
+    if constexpr (R == 1 && PASS2) kind = STAGE_EULER;
     extern __shared__ __align__(128) float smem[];
     const int N1 = CT ? CN1 : a.N1;
     const int RSZ = CT ? geo_rsz(R, CN1, CB) : a.RSZ;
@@ -924,6 +927,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                     if constexpr (!PASS2) inc_val(dL, mn[MA], mx[MA]);
                 }
             }
+
             float2 vnv = f2s(0.f), ttv = f2s(0.f);         // Vn / target of the current step (pass 2), loaded a step ahead
             if constexpr (PASS2) {                         // (unless staged by TMA with the step's tiles: xs)
                 if (act) {
@@ -935,10 +939,16 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
             }
 
             long long gi = U.cbase + (long long)(m0 - mlo) * M + grow * N1 + qc0;   // element of node 0 (this step)
+#if ODP_MARCH_UNROLL == 2
+#pragma unroll 2
+#elif ODP_MARCH_UNROLL == 3
+#pragma unroll 3
+#endif
             for (int jg = m0; jg < m1; ++jg, ++it, gi += M) {
                 // window value entering at this step: v_{j+R} (ring inside the segment, else global / ghost)
                 const int kin = jg + R;
                 const bool in_ring = kin < m1;
+
                 float2 vin = f2s(0.f);
                 if (act && !in_ring) {
                     if (mper || kin < Nm) {

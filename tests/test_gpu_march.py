@@ -102,3 +102,38 @@ def test_march_matches_stream_bits_of_range(acc):
     b, ib = run_gpu(w, V0, kernel="stream")
     assert ia["steps"] == ib["steps"] and ia["tau_reached"] == ib["tau_reached"]
     assert np.abs(a - b).max() <= 2e-6
+
+
+@pytest.mark.parametrize("mode", ["brt", "brs"])
+@pytest.mark.parametrize("N", [(6, 5, 7, 6, 6, 8), (3, 4, 3, 5, 48, 48), (5, 6, 74, 14)],
+                         ids=["dint6-generic", "dint6-c5-instance", "car4-ragged-rows"])
+def test_low_target_staging_is_bitwise(N, mode):
+    # LOW pass 2 stages the target by TMA with the step's tiles (MarchArgs::xs); with
+    # ODP_MARCH_XS=0 it reads it per thread one step ahead.  Same float32 operations: identical bits.
+    # (3, 4, 3, 5, 48, 48) runs the shape-specialised c5 instance; 74 rows in blocks of 16 leave a
+    # ragged last row block (10 rows: a shorter target copy).
+    if len(N) == 6:
+        w = Workload("dint6", N, (-4.0, -2.0) * 3, (4.0, 2.0) * 3, (0,) * 6, "DOUBLEINT6D", (1.0, 0.2, -1.0),
+                     (0.0, 0.03, 0.06), "low", 0.8, mode, ("random_smooth", 6))
+    else:
+        w = Workload("car4", N, (-5.0, -5.0, 0.0, -math.pi), (5.0, 5.0, 4.0, math.pi), (0, 0, 0, 1), "CAR4D",
+                     (1.5, 1.0, 0.25, 0.25, -1.0), (0.0, 0.05, 0.1), "low", 0.8, mode, ("random_smooth", 4))
+    V0 = noise_v0(N, 3)
+    old, old_b = os.environ.get("ODP_MARCH_XS"), os.environ.get("ODP_MARCH_B")
+    try:
+        if len(N) == 4:
+            os.environ["ODP_MARCH_B"] = "16"
+        os.environ.pop("ODP_MARCH_XS", None)
+        a, ia = run_gpu(w, V0, kernel="march")
+        os.environ["ODP_MARCH_XS"] = "0"
+        b, ib = run_gpu(w, V0, kernel="march")
+    finally:
+        for k, v in (("ODP_MARCH_XS", old), ("ODP_MARCH_B", old_b)):
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    assert ia["steps"] == ib["steps"] and ia["stages"] == ib["stages"]
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    ref = run_oracle(w, V0)
+    assert_parity(a, ref.out, what=f"{w.name} {mode} staged target")
