@@ -1266,6 +1266,9 @@ MarchFnsAll march_fns() {
 #endif
             march_add<F, NDIM, R, 48, 16, 2>(t);
             if constexpr (R == 1) march_add<F, NDIM, R, 48, 16, 4>(t);   // c5 LOW
+#ifdef ODP_MARCH_XINST             // smaller row blocks: 3 CTAs/SM for c5 LOW (ODP_MARCH_B=12 / 8)
+            if constexpr (R == 1) { march_add<F, NDIM, R, 48, 12, 4>(t); march_add<F, NDIM, R, 48, 8, 4>(t); }
+#endif
         } else if constexpr (std::is_same<F, FCar5D>::value && R == 2) {   // c3
             march_add<F, NDIM, R, 40, 20, 2>(t);
             march_add<F, NDIM, R, 40, 20, 3>(t);
