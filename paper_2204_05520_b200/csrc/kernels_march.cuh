@@ -74,6 +74,9 @@ namespace odp {
 #ifndef ODP_MARCH_SLEEP_NS
 #define ODP_MARCH_SLEEP_NS 64   // back-off of the ODP_MARCH_WAIT = 0 wait loop
 #endif
+#ifndef ODP_MARCH_KINDS
+#define ODP_MARCH_KINDS 1      // MEDIUM shape-specialised pass 2 compiled per RK stage kind (0: runtime kind)
+#endif
 #ifndef ODP_MARCH_UNROLL
 #define ODP_MARCH_UNROLL 1     // experiment: unroll the marching loop (window shifts become renames)
 #endif
@@ -500,8 +503,9 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) 
 
 // LBT / LBM: the launch bounds (threads per CTA, CTAs per SM) the register budget is sized for;
 // shape-specialised instances with fewer rows per block may set them to their own block size
+// KIND >= 0: pass 2 compiled for one stage kind (Euler / RK stage 1 / RK stage 2), -1: runtime `kind`
 template <class F, int NDIM, int R, int NP, bool PASS2, int CN1 = 0, int CB = 0, int NST = 2,
-          int LBT = MARCH_MAXT1, int LBM = ODP_MARCH_MINB1>
+          int LBT = MARCH_MAXT1, int LBM = ODP_MARCH_MINB1, int KIND = -1>
 __global__ void __launch_bounds__(LBT, LBM)
 k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, const float *__restrict__ T,
         float *out, float *partials, const DevState *st, FParams fp, int kind, int brt) {
@@ -528,6 +532,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     const int dbg = MARCH_EXP ? a.dbg : 0;
     // LOW (R = 1) is always forward Euler (odp.cu's step sequence); MEDIUM runs RK stages 1 and 2
     if constexpr (R == 1 && PASS2) kind = STAGE_EULER;
+    if constexpr (KIND >= 0 && PASS2) kind = KIND;
     extern __shared__ __align__(128) float smem[];
     const int N1 = CT ? CN1 : a.N1;
     const int RSZ = CT ? geo_rsz(R, CN1, CB) : a.RSZ;
@@ -1220,6 +1225,7 @@ typedef void (*march_fn)(MarchArgs, GridDev, const float *, const float *, const
 struct MarchInst {
     int n1 = 0, b = 0, nst = 2;
     march_fn pass1 = nullptr, pass2 = nullptr;
+    march_fn pass2k[3] = {nullptr, nullptr, nullptr};   // per stage kind (null: pass2 with the runtime kind)
 };
 constexpr int MARCH_MAX_INST = 12;
 struct MarchFnsAll {
@@ -1229,6 +1235,7 @@ struct MarchFnsAll {
 };
 struct MarchFns {
     march_fn pass1 = nullptr, pass2 = nullptr;
+    march_fn pass2k[3] = {nullptr, nullptr, nullptr};
     int specialised = 0;
 };
 struct MarchPlan {
@@ -1246,6 +1253,12 @@ void march_add(MarchFnsAll &t) {
         m.n1 = CN1; m.b = CB; m.nst = NST;
         m.pass1 = k_march<F, NDIM, R, 1, false, CN1, CB, NST, LBT, LBM>;
         m.pass2 = k_march<F, NDIM, R, 1, true, CN1, CB, NST, LBT, LBM>;
+#if ODP_MARCH_KINDS
+        if constexpr (R == 2) {      // MEDIUM: the RK stage 1 launch carries no Vn / target code at all
+            m.pass2k[STAGE_RK1] = k_march<F, NDIM, R, 1, true, CN1, CB, NST, LBT, LBM, STAGE_RK1>;
+            m.pass2k[STAGE_RK2] = k_march<F, NDIM, R, 1, true, CN1, CB, NST, LBT, LBM, STAGE_RK2>;
+        }
+#endif
     }
 }
 
@@ -1345,6 +1358,7 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
         if (all.inst[i].n1 == N1 && all.inst[i].b == best && all.inst[i].nst == nst) {
             fns->pass1 = all.inst[i].pass1;
             fns->pass2 = all.inst[i].pass2;
+            for (int k = 0; k < 3; ++k) fns->pass2k[k] = all.inst[i].pass2k[k];
             fns->specialised = 1;
         }
     MarchArgs &a = p->a;
@@ -1421,8 +1435,8 @@ inline bool march_plan(const GridDev &g, int R, const MarchFnsAll &all, const vo
 inline int march_prepare(const MarchFns &t, MarchPlan &p, int nsm) {
     int occ1 = 0, occ2 = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
-        for (march_fn fn : {t.pass1, t.pass2}) {
-            if (cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) != cudaSuccess)
+        for (march_fn fn : {t.pass1, t.pass2, t.pass2k[0], t.pass2k[1], t.pass2k[2]}) {
+            if (fn && cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem) != cudaSuccess)
                 return 1;
         }
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, (const void *)t.pass1, p.block, p.smem) != cudaSuccess) return 1;
@@ -1461,7 +1475,8 @@ inline void march_pass2(const MarchFns &t, const MarchPlan &p, const GridDev &g,
     a.xs = 0;
     if (a.xn >= 2) a.xs = need;
     else if (a.xn == 1) a.xs = (need & 1) ? 1 : need;
-    t.pass2<<<p.grid, p.block, p.smem, s>>>(a, g, W, Vn, T, out, guard_partials, st, fp, kind, brt);
+    const march_fn fn = (kind >= 0 && kind < 3 && t.pass2k[kind]) ? t.pass2k[kind] : t.pass2;
+    fn<<<p.grid, p.block, p.smem, s>>>(a, g, W, Vn, T, out, guard_partials, st, fp, kind, brt);
 }
 
 // Pass 1 split by axis-0 planes (multi-GPU overlap): the interior planes [R, N0 - R)
