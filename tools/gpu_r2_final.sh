@@ -12,5 +12,4 @@ bash tools/bench_configs.sh > gpurun_out/${T}_configs.txt 2>&1; cat gpurun_out/$
 python tools/profile_run.py c4 0.05 > gpurun_out/plain_launch.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${T}_launches.csv python tools/profile_run.py c4 0.05 > gpurun_out/ncu_launches.log 2>&1
 tail -1 gpurun_out/ncu_launches.log
-# geometry probe: generic instance, B = 30 (2 CTAs/SM) vs B = 15 / 10 (smaller stages: more CTAs/SM)
-for B in 30 15 10 6; do echo "generic B=$B $(ODP_MARCH_VERBOSE=1 ODP_MARCH_GENERIC=1 ODP_MARCH_B=$B timeout 300 python tools/kbench.py c4 0.05 2>&1 | grep -E 'plan|stages' | sort -u | tr '\n' ' ')"; done 2>&1 | tee gpurun_out/${T}_geo.log
+
