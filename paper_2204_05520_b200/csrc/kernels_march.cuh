@@ -77,6 +77,9 @@ namespace odp {
 #ifndef ODP_MARCH_KINDS
 #define ODP_MARCH_KINDS 1      // MEDIUM shape-specialised pass 2 compiled per RK stage kind (0: runtime kind)
 #endif
+#ifndef ODP_MARCH_LDSTEP
+#define ODP_MARCH_LDSTEP 1     // RK-stage-2 instances load Vn / T per step instead of one step ahead (0: off)
+#endif
 #ifndef ODP_MARCH_UNROLL
 #define ODP_MARCH_UNROLL 1     // experiment: unroll the marching loop (window shifts become renames)
 #endif
@@ -533,6 +536,9 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
     // LOW (R = 1) is always forward Euler (odp.cu's step sequence); MEDIUM runs RK stages 1 and 2
     if constexpr (R == 1 && PASS2) kind = STAGE_EULER;
     if constexpr (KIND >= 0 && PASS2) kind = KIND;
+    // RK stage 2 instances load Vn / T at the start of each step (no loop-carried registers); the
+    // others keep the one-step-ahead load (DESIGN.md §7 third table)
+    constexpr bool LDSTEP = ODP_MARCH_LDSTEP && KIND == STAGE_RK2;
     extern __shared__ __align__(128) float smem[];
     const int N1 = CT ? CN1 : a.N1;
     const int RSZ = CT ? geo_rsz(R, CN1, CB) : a.RSZ;
@@ -934,7 +940,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
             }
 
             float2 vnv = f2s(0.f), ttv = f2s(0.f);         // Vn / target of the current step (pass 2), loaded a step ahead
-            if constexpr (PASS2) {                         // (unless staged by TMA with the step's tiles: xs)
+            if constexpr (PASS2 && !LDSTEP) {              // (unless staged by TMA with the step's tiles: xs)
                 if (act) {
                     const long long gi0 = U.cbase + (long long)(m0 - mlo) * M + grow * N1 + qc0;
                     ODP_CHK(gi0 >= 0 && gi0 + 2 <= g.P, 41, gi0, g.P);
@@ -953,6 +959,13 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                 // window value entering at this step: v_{j+R} (ring inside the segment, else global / ghost)
                 const int kin = jg + R;
                 const bool in_ring = kin < m1;
+                if constexpr (PASS2 && LDSTEP) {           // this step's Vn / target, before the copy wait
+                    if (act) {
+                        ODP_CHK(gi >= 0 && gi + 2 <= g.P, 41, gi, g.P);
+                        if (kind == STAGE_RK2 && !(xs & 2)) vnv = *reinterpret_cast<const float2 *>(Vn + gi);
+                        if (brt && kind != STAGE_RK1 && !(xs & 1)) ttv = __ldg(reinterpret_cast<const float2 *>(T + gi));
+                    }
+                }
 
                 float2 vin = f2s(0.f);
                 if (act && !in_ring) {
@@ -1174,7 +1187,7 @@ k_march(MarchArgs a, GridDev g, const float *__restrict__ W, const float *Vn, co
                         ODP_CHK(gi >= 0 && gi + 2 <= g.P, 42, gi, g.P);
                         *reinterpret_cast<float2 *>(out + gi) = v;
                         mabs = max3nan(mabs, fabsf(v.x), fabsf(v.y));   // output guard (single-pass solves)
-                        if (jg + 1 < m1) {                    // the next step's Vn / target
+                        if (!LDSTEP && jg + 1 < m1) {         // the next step's Vn / target
                             if (kind == STAGE_RK2 && !(xs & 2)) vnv = *reinterpret_cast<const float2 *>(Vn + gi + M);
                             if (brt && kind != STAGE_RK1 && !(xs & 1)) ttv = __ldg(reinterpret_cast<const float2 *>(T + gi + M));
                         }
