@@ -224,7 +224,7 @@ __device__ __forceinline__ void finalize_body(const float *partials, int nparts,
     } else if constexpr (F::DEPS3) {   // alpha_d depends on 3 coordinates: per-CTA maxima from k_amax3
         if (threadIdx.x < NDIM) {
             float a = 0.f;
-            for (int p = 0; p < namax; ++p) a = fmaxf(a, amax_parts[p * NDIM + threadIdx.x]);
+            for (int p = 0; p < namax; ++p) a = fmaxf(a, ldw<CG>(amax_parts + p * NDIM + threadIdx.x));
             am[threadIdx.x] = a;
         }
         __syncthreads();
@@ -296,21 +296,15 @@ __global__ void k_force_active(DevState *st) { force_active_body(st); }
 // stored first (k_store_range: the same exact min/max reduction as k_finalize), then k_amax3 takes
 // the maximum of alpha_{i,d} over the nodes of that coordinate grid with many CTAs (the
 // one-CTA enumeration of k_finalize would cost N0 N1 N2 / 256 iterations per stage).
-template <int NDIM>
-__global__ void __launch_bounds__(256) k_store_range(const float *__restrict__ partials, int nparts, DevState *st,
-                                                     const float *__restrict__ range) {
-    if (!st->active) return;
+template <int NDIM, bool CG>
+__device__ __forceinline__ void store_range_body(const float *partials, int nparts, DevState *st) {
     constexpr int Q = 2 * NDIM + 2;
     __shared__ float red[Q][8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (range) {
-        if (threadIdx.x < NDIM) { st->minD[threadIdx.x] = -range[threadIdx.x]; st->maxD[threadIdx.x] = range[NDIM + threadIdx.x]; }
-        return;
-    }
     for (int q = 0; q < 2 * NDIM; ++q) {
         float r = q < NDIM ? __int_as_float(0x7f800000) : -__int_as_float(0x7f800000);
         for (int p = threadIdx.x; p < nparts; p += blockDim.x) {
-            const float o = partials[(long long)p * Q + q];
+            const float o = ldw<CG>(partials + (long long)p * Q + q);
             r = q < NDIM ? fminf(r, o) : fmaxf(r, o);
         }
 #pragma unroll
@@ -329,9 +323,19 @@ __global__ void __launch_bounds__(256) k_store_range(const float *__restrict__ p
     }
 }
 
-template <class F, int NDIM>
-__global__ void __launch_bounds__(256) k_amax3(GridDev g, FParams fp, const DevState *st, float *parts) {
+template <int NDIM>
+__global__ void __launch_bounds__(256) k_store_range(const float *__restrict__ partials, int nparts, DevState *st,
+                                                     const float *__restrict__ range) {
     if (!st->active) return;
+    if (range) {
+        if (threadIdx.x < NDIM) { st->minD[threadIdx.x] = -range[threadIdx.x]; st->maxD[threadIdx.x] = range[NDIM + threadIdx.x]; }
+        return;
+    }
+    store_range_body<NDIM, false>(partials, nparts, st);
+}
+
+template <class F, int NDIM>
+__device__ __forceinline__ void amax3_body(const GridDev &g, const FParams &fp, const DevState *st, float *parts) {
     F f;
     f.init(fp, st->minD, st->maxD);
     float a[NDIM];
@@ -364,6 +368,12 @@ __global__ void __launch_bounds__(256) k_amax3(GridDev g, FParams fp, const DevS
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = fmaxf(r, red[threadIdx.x][w]);
         parts[blockIdx.x * NDIM + threadIdx.x] = r;
     }
+}
+
+template <class F, int NDIM>
+__global__ void __launch_bounds__(256) k_amax3(GridDev g, FParams fp, const DevState *st, float *parts) {
+    if (!st->active) return;
+    amax3_body<F, NDIM>(g, fp, st, parts);
 }
 
 // Single-pass solves: for a functor whose alpha_(i,d) does not depend on the
@@ -445,6 +455,7 @@ __global__ void k_advance(DevState *st) { advance_body(st); }
 // CTA 0 writes the state back at the end.  Launched with cudaLaunchCooperativeKernel (all CTAs
 // co-resident, required by the spin barrier).
 // ------------------------------------------------------------------------------------------------
+constexpr int ODP_AMAX_PARTS = 4096;   // per-CTA alpha^max records (k_amax3: nsm CTAs; k_resident: its grid)
 struct ResidentArgs {
     float *buf0, *buf1;          // V ping-pong (local slab layout, no halo use: one rank)
     const float *T;              // BRT target
@@ -455,6 +466,7 @@ struct ResidentArgs {
     const double *dxd;
     DevState *st;
     unsigned *bar;               // grid barrier counter, zeroed before the launch
+    float *amax_parts;           // DEPS3 functors: per-CTA alpha^max, gridDim.x * n floats
     int low, brt;
 };
 
@@ -493,8 +505,19 @@ __global__ void __launch_bounds__(256) k_resident(GridDev g, FParams fp, Residen
     };
     bool have_amax = false;                     // RANGE_FREE: alpha^max computed once (bitwise the same)
     auto fin = [&](int stage, int final_check) {
-        finalize_body<F, NDIM, true>(a.partials, np, &sst, g, fp, a.dxd, stage, final_check, nullptr, nullptr, 0,
-                                     have_amax);
+        if constexpr (F::DEPS3) {
+            // alpha_d depends on 3 coordinates (Eq. 7): k_store_range + k_amax3 of the multi-launch
+            // path, here by every CTA over its share of the coordinate grid, one more grid barrier;
+            // the branch is uniform over the grid (every CTA holds the same state)
+            if (stage == 0 && !final_check && sst.active) {
+                store_range_body<NDIM, true>(a.partials, np, &sst);
+                __syncthreads();
+                amax3_body<F, NDIM>(g, fp, &sst, a.amax_parts);
+                grid_barrier(a.bar, gen);
+            }
+        }
+        finalize_body<F, NDIM, true>(a.partials, np, &sst, g, fp, a.dxd, stage, final_check, nullptr, a.amax_parts,
+                                     F::DEPS3 ? np : 0, have_amax);
         __syncthreads();
         if (stage == 0 && !final_check && sst.active) have_amax = true;
     };
@@ -561,7 +584,7 @@ struct KernelSet {
     guard_fn guard = nullptr;
     srange_fn srange = nullptr;   // DEPS3 functors only
     amax3_fn amax3 = nullptr;
-    res_fn res = nullptr;         // k_resident (not for DEPS3 functors: their alpha^max is grid-wide)
+    res_fn res = nullptr;         // k_resident
     bool range_free = false;
     TiledFns tiled;      // tiled family (may be empty)
     StreamFnsAll stream; // stream family (may be empty)
@@ -580,9 +603,8 @@ static KernelSet make_set() {
     if constexpr (F::DEPS3) {
         k.srange = k_store_range<NDIM>;
         k.amax3 = k_amax3<F, NDIM>;
-    } else {
-        k.res = k_resident<F, NDIM, R>;
     }
+    k.res = k_resident<F, NDIM, R>;
     if constexpr (F::SEPARABLE) {      // the tiled / stream families assemble separable Hamiltonians only
         k.tiled = tiled_fns<F, NDIM, R>();
         k.stream = stream_fns<F, NDIM, R>();
@@ -851,7 +873,7 @@ static odp_status ensure_device(odp_grid *g, int nparts_needed) {
         g->max_parts = nparts_needed;
     }
     if (!g->d_range) CUDA_TRY(cudaMalloc(&g->d_range, (2 * MAXD + 2) * sizeof(float)));
-    if (!g->d_amax) CUDA_TRY(cudaMalloc(&g->d_amax, 1024 * MAXD * sizeof(float)));
+    if (!g->d_amax) CUDA_TRY(cudaMalloc(&g->d_amax, ODP_AMAX_PARTS * MAXD * sizeof(float)));
     return ODP_OK;
 }
 
@@ -1193,8 +1215,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
     const bool res_ok = ks.res && g->nranks == 1 && !g->comm && !g->lb && !(opts && opts->kernel_ms) &&
                         !(opts && opts->single_pass);
     if (want_kernel == ODP_KERNEL_RESIDENT && !res_ok)
-        return fail(ODP_EINVAL, "resident kernel: one rank, no kernel_ms / single_pass, and a dynamics whose alpha^max "
-                                "enumerates <= 2 axes");
+        return fail(ODP_EINVAL, "resident kernel: one rank, no kernel_ms / single_pass");
     const bool use_resident = want_kernel == ODP_KERNEL_RESIDENT ||
                               (want_kernel == ODP_KERNEL_AUTO && res_ok && local_points(g) <= res_max);
     if (use_resident) use_march = use_stream = use_tiled = false;
@@ -1263,7 +1284,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
         int occ = 0;
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.res, block, 0));
         if (occ < 1) return fail(ODP_ECUDA, "k_resident does not fit on an SM");
-        long long nb = std::min<long long>(want_blocks, (long long)occ * nsm);
+        long long nb = std::min<long long>(std::min<long long>(want_blocks, (long long)occ * nsm), ODP_AMAX_PARTS);
         if (getenv("ODP_RESIDENT_CTAS")) nb = std::max(1LL, std::min<long long>(nb, atoll(getenv("ODP_RESIDENT_CTAS"))));
         if ((st = ensure_device(g, (int)nb))) return st;
         if (g->tau_cap < ntau) {
@@ -1279,6 +1300,7 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
         ResidentArgs ra;
         ra.buf0 = buf[0]; ra.buf1 = buf[1]; ra.T = T; ra.out = out; ra.tau = g->d_tau; ra.ntau = ntau;
         ra.k_out0 = k_out; ra.partials = g->d_partials; ra.dxd = g->d_dx; ra.st = g->d_state; ra.bar = g->d_bar;
+        ra.amax_parts = g->d_amax;
         ra.low = accuracy == ODP_LOW; ra.brt = brt;
         void *kargs[] = {&gd, &fp, &ra};
         NvtxRange nv("odp k_resident (whole solve)");

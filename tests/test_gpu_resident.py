@@ -18,6 +18,7 @@ CASES = [
     ("c2", (14, 12, 11, 13)),
     ("c3", (11, 10, 12, 9, 8)),
     ("c4", (8, 7, 8, 6, 7, 9)),
+    ("f2", (14, 12, 11)),                              # Eq. 7: alpha^max over 3 coordinates (k_amax3 body)
 ]
 
 
@@ -82,14 +83,29 @@ def test_resident_numeric_failure_matches_the_generic_family():
     assert (ia["steps"], ia["stages"], ia["tau_reached"]) == (ib["steps"], ib["stages"], ib["tau_reached"])
 
 
-def test_resident_refuses_where_it_does_not_apply():
+def test_resident_pair_dubins_against_the_oracle():
+    # Eq. 7: alpha_d depends on (x, y, theta), so every step's alpha^max is the
+    # grid-wide maximum k_amax3 takes -- inside the one launch, after one more grid barrier
     import torch
     import paper_2204_05520_b200 as odp
     w = Workload("pd", (12, 11, 10), (-6.0, -10.0, -math.pi), (20.0, 10.0, math.pi), (0, 0, 1), "PAIR_DUBINS3D",
-                 (5.0, 5.0, 1.0, 1.0, 1.0), (0.0, 0.1), "low", 0.8, "brt", ("cylinder", (0, 1), 5.0))
-    V0 = torch.from_numpy(make_v0(w)).cuda()
-    with pytest.raises(odp.OdpError, match="resident"):
-        odp.solve_workload(w, V0, kernel="resident")
+                 (5.0, 5.0, 1.0, 1.0, 1.0), (0.0, 0.1, 0.4), "low", 0.8, "brt", ("cylinder", (0, 1), 5.0))
+    V0 = make_v0(w)
+    g = odp.Grid(w.N, w.lo, w.hi, w.periodic_mask)
+    out, info = odp.hj_solve(g, w.dynamics, w.params, torch.from_numpy(V0).cuda(), w.tau, w.accuracy, w.mode,
+                             cfl=w.cfl)                                   # AUTO picks resident here
+    torch.cuda.synchronize()
+    assert g.launch_count() == 2
+    ref = run_oracle(w, V0)
+    assert_parity(out.cpu().numpy(), ref.out, what="pair-dubins resident")
+    assert info["steps"] == ref.steps and info["stages"] == ref.stages
+    b, _ = odp.solve_workload(w, torch.from_numpy(V0).cuda(), kernel="generic")
+    assert torch.equal(out, b)
+
+
+def test_resident_refuses_where_it_does_not_apply():
+    import torch
+    import paper_2204_05520_b200 as odp
     w1 = _case("c2", (14, 12, 11, 13), "low")
     V1 = torch.from_numpy(make_v0(w1)).cuda()
     with pytest.raises(odp.OdpError, match="resident"):
