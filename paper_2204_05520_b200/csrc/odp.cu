@@ -222,10 +222,23 @@ __device__ __forceinline__ void finalize_body(const float *partials, int nparts,
         if (threadIdx.x < NDIM) am[threadIdx.x] = st->amax[threadIdx.x];   // previous step's, bit for bit
         __syncthreads();
     } else if constexpr (F::DEPS3) {   // alpha_d depends on 3 coordinates: per-CTA maxima from k_amax3
+        float a[NDIM];                  // block-wide max over the records (exact in any order)
+#pragma unroll
+        for (int d = 0; d < NDIM; ++d) a[d] = 0.f;
+        for (int p = threadIdx.x; p < namax; p += blockDim.x)
+#pragma unroll
+            for (int d = 0; d < NDIM; ++d) a[d] = fmaxf(a[d], ldw<CG>(amax_parts + p * NDIM + d));
+#pragma unroll
+        for (int d = 0; d < NDIM; ++d) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) a[d] = fmaxf(a[d], __shfl_xor_sync(0xffffffffu, a[d], off));
+            if (lane == 0) red[d][warp] = a[d];
+        }
+        __syncthreads();
         if (threadIdx.x < NDIM) {
-            float a = 0.f;
-            for (int p = 0; p < namax; ++p) a = fmaxf(a, ldw<CG>(amax_parts + p * NDIM + threadIdx.x));
-            am[threadIdx.x] = a;
+            float r = red[threadIdx.x][0];
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) r = fmaxf(r, red[threadIdx.x][w]);
+            am[threadIdx.x] = r;
         }
         __syncthreads();
     } else
@@ -374,6 +387,32 @@ template <class F, int NDIM>
 __global__ void __launch_bounds__(256) k_amax3(GridDev g, FParams fp, const DevState *st, float *parts) {
     if (!st->active) return;
     amax3_body<F, NDIM>(g, fp, st, parts);
+}
+
+// One launch in place of k_store_range + k_amax3 + k_finalize (one rank, stage 0 of a step): every
+// CTA reduces pass 1's partials into a CTA-local range (the same exact min/max), takes its share of
+// the alpha^max enumeration, and the LAST CTA to finish (arrival counter, reset by that CTA) runs the
+// finalize on the global state, reading the per-CTA maxima through L2.  Bitwise the three launches.
+template <class F, int NDIM>
+__global__ void __launch_bounds__(256) k_amax3_fin(const float *__restrict__ partials, int nparts, DevState *st,
+                                                   GridDev g, FParams fp, const double *__restrict__ dxd,
+                                                   float *parts, unsigned *ctr) {
+    if (!st->active) return;
+    __shared__ DevState loc;
+    __shared__ bool last;
+    store_range_body<NDIM, false>(partials, nparts, &loc);
+    __syncthreads();
+    amax3_body<F, NDIM>(g, fp, &loc, parts);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+        if (last) *ctr = 0u;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    finalize_body<F, NDIM, true>(partials, nparts, st, g, fp, dxd, 0, 0, nullptr, parts, (int)gridDim.x);
 }
 
 // Single-pass solves: for a functor whose alpha_(i,d) does not depend on the
@@ -572,6 +611,7 @@ typedef void (*fin_fn)(const float *, int, DevState *, GridDev, FParams, const d
                        const float *, int);
 typedef void (*srange_fn)(const float *, int, DevState *, const float *);
 typedef void (*amax3_fn)(GridDev, FParams, const DevState *, float *);
+typedef void (*amax3fin_fn)(const float *, int, DevState *, GridDev, FParams, const double *, float *, unsigned *);
 typedef void (*red_fn)(const float *, int, const DevState *, float *);
 typedef void (*guard_fn)(const float *, int, DevState *, const float *, int);
 typedef void (*res_fn)(GridDev, FParams, ResidentArgs);
@@ -584,6 +624,7 @@ struct KernelSet {
     guard_fn guard = nullptr;
     srange_fn srange = nullptr;   // DEPS3 functors only
     amax3_fn amax3 = nullptr;
+    amax3fin_fn amax3fin = nullptr;   // DEPS3, one rank: range + alpha^max + finalize in one launch
     res_fn res = nullptr;         // k_resident
     bool range_free = false;
     TiledFns tiled;      // tiled family (may be empty)
@@ -603,6 +644,7 @@ static KernelSet make_set() {
     if constexpr (F::DEPS3) {
         k.srange = k_store_range<NDIM>;
         k.amax3 = k_amax3<F, NDIM>;
+        k.amax3fin = k_amax3_fin<F, NDIM>;
     }
     k.res = k_resident<F, NDIM, R>;
     if constexpr (F::SEPARABLE) {      // the tiled / stream families assemble separable Hamiltonians only
@@ -661,6 +703,7 @@ struct odp_grid {
     double *d_tau = nullptr;      // k_resident: device copy of the save times (capacity tau_cap)
     int tau_cap = 0;
     unsigned *d_bar = nullptr;    // k_resident: grid barrier counter
+    unsigned *d_ctr = nullptr;    // k_amax3_fin: arrival counter (zero between launches)
     // device cache (allocated lazily on the device current at the first solve)
     int device = -1;
     float *d_tab = nullptr;
@@ -700,8 +743,8 @@ static void free_device(odp_grid *g) {
     if (g->h_ttr) cudaFreeHost(g->h_ttr);
     cudaFree(g->d_stage);
     g->d_stage = nullptr; g->stage_elems = 0;
-    cudaFree(g->d_tau); cudaFree(g->d_bar);
-    g->d_tau = nullptr; g->tau_cap = 0; g->d_bar = nullptr;
+    cudaFree(g->d_tau); cudaFree(g->d_bar); cudaFree(g->d_ctr);
+    g->d_tau = nullptr; g->tau_cap = 0; g->d_bar = nullptr; g->d_ctr = nullptr;
     g->d_ttr = nullptr; g->h_ttr = nullptr;
     if (g->own_stream) cudaStreamDestroy(g->own_stream);
     if (g->side_stream) cudaStreamDestroy(g->side_stream);
@@ -1357,13 +1400,24 @@ static odp_status solve_device(odp_grid *g, int dyn, const double *params, int n
     auto exch = [&](float *Wx) {
         if (g->nranks > 1 && cst == ODP_OK) cst = halo_exchange(g, Wx, R, s);
     };
-    const int namax = ks.amax3 ? nsm : 0;           // k_amax3 CTAs (DEPS3 functors)
+    // k_amax3 CTAs (DEPS3 functors): 3 per SM -- the enumeration is a chain of dependent table loads
+    // per node, latency-bound at one CTA per SM (f2 100^3: ~27 nodes per thread); f2 sweep of
+    // ODP_AMAX3_CPS 1/2/3/4/6/8/16: 26.1/29.3/30.0/29.7/27.0/26.8/21.7 Gpt-st/s
+    const int namax = ks.amax3 ? std::min(ODP_AMAX_PARTS, nsm * (getenv("ODP_AMAX3_CPS") ? std::max(1, atoi(getenv("ODP_AMAX3_CPS"))) : 3)) : 0;
+    if (ks.amax3fin && !g->d_ctr) {
+        CUDA_TRY(cudaMalloc(&g->d_ctr, sizeof(unsigned)));
+        CUDA_TRY(cudaMemsetAsync(g->d_ctr, 0, sizeof(unsigned), s));
+    }
     auto launch_fin = [&](int stage_in_step, int final_check) {
         const float *rng = nullptr;
         if (g->comm || g->lb) {
             ks.red<<<1, 256, 0, s>>>(g->d_partials, nparts1, g->d_state, g->d_range);
             if (cst == ODP_OK) cst = range_allreduce(g, n, s);
             rng = g->d_range;
+        }
+        if (ks.amax3fin && !rng && stage_in_step == 0 && !final_check && !getenv("ODP_AMAX3_SPLIT")) {
+            ks.amax3fin<<<namax, 256, 0, s>>>(g->d_partials, nparts1, g->d_state, gd, fp, g->d_dx, g->d_amax, g->d_ctr);
+            return;
         }
         if (ks.amax3 && stage_in_step == 0 && !final_check) {
             ks.srange<<<1, 256, 0, s>>>(g->d_partials, nparts1, g->d_state, rng);
